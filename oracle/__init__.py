@@ -1,0 +1,158 @@
+"""TEST INFRASTRUCTURE ONLY -- the CPU oracle for the SWR solve (arXiv 1306.4596).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference``) may import this package.  The
+product path (``paper_1306_4596_b200``) never imports it and shares no code
+with it; it takes its inputs from ``kfp_inputs`` like the CUDA path does.
+
+Contents
+--------
+* ``kfp_oracle.c`` (built into ``liborc.so``): the plain fp64 step-by-step
+  monodomain + Jacobi SWR solver (see its header for the paper passages).
+* ``modal.py``: the mode-reduced oracle for the manufactured-solution configs
+  (a special case that reduces the 2-D scheme to one complex 1-D recurrence
+  per step, solved with LAPACK's banded solver).
+* ``dense.py``: brute-force dense space-time assemblies for tiny grids.
+
+Parity status per function: every function here is pinned by
+``tests/test_oracle_pins.py``; none is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "kfp_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liborc.so")
+_lock = threading.Lock()
+_lib = None
+
+KIND = {"dirichlet": 0, "robin": 1}
+END_PHYS, END_DIRICHLET, END_ROBIN = 0, 1, 2
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle (gcc, -O2, OpenMP over x-columns)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-fopenmp", "-shared", "-fPIC", "-o", _LIB_PATH, _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+    return _LIB_PATH
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [
+        ("nx", ctypes.c_int32), ("nv", ctypes.c_int32), ("nt", ctypes.c_int32),
+        ("vmax", ctypes.c_double), ("t_final", ctypes.c_double),
+        ("f_rank", ctypes.c_int32),
+        ("ft", ctypes.c_void_p), ("fv", ctypes.c_void_p), ("fx", ctypes.c_void_p),
+        ("u0_rank", ctypes.c_int32),
+        ("u0v", ctypes.c_void_p), ("u0x", ctypes.c_void_p),
+    ]
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB_PATH)
+            P = ctypes.POINTER(_Problem)
+            dp = ctypes.c_void_p
+            lib.orc_num_threads.restype = ctypes.c_int
+            lib.orc_subdomains.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp]
+            lib.orc_monodomain.argtypes = [P, ctypes.c_int, dp, dp, dp]
+            lib.orc_window.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                       dp, dp, ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, dp,
+                                       ctypes.c_int, dp, dp, dp]
+            lib.orc_swr.argtypes = [P, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    dp, dp, dp, dp, dp, dp]
+            _lib = lib
+    return _lib
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+class _Bound:
+    """Keeps the numpy tables alive while the C struct points at them."""
+
+    def __init__(self, prob):
+        g = prob.grid
+        self.arrays = [np.ascontiguousarray(x, dtype=np.float64) for x in (prob.ft, prob.fv, prob.fx, prob.u0v, prob.u0x)]
+        ft, fv, fx, u0v, u0x = self.arrays
+        self.s = _Problem(g.nx, g.nv, g.nt, g.vmax, g.t_final, prob.f_rank,
+                          _ptr(ft), _ptr(fv), _ptr(fx), prob.u0_rank, _ptr(u0v), _ptr(u0x))
+
+    def ref(self):
+        return ctypes.byref(self.s)
+
+
+def num_threads() -> int:
+    return int(_load().orc_num_threads())
+
+
+def subdomains(nv: int, n_sub: int, overlap: int):
+    lo = np.zeros(n_sub, np.int32)
+    hi = np.zeros(n_sub, np.int32)
+    if _load().orc_subdomains(nv, n_sub, overlap, _ptr(lo), _ptr(hi)) != 0:
+        raise ValueError("invalid decomposition")
+    return lo, hi
+
+
+def monodomain(prob, rec_nodes=()):
+    """U(T) [(nv+1), nx] and U at rec_nodes for n=1..nt ([len, nt, nx])."""
+    g = prob.grid
+    b = _Bound(prob)
+    nodes = np.ascontiguousarray(rec_nodes, dtype=np.int32)
+    rec = np.zeros((max(len(nodes), 1), g.nt, g.nx))
+    UT = np.zeros((g.nv + 1, g.nx))
+    _load().orc_monodomain(b.ref(), len(nodes), _ptr(nodes), _ptr(rec), _ptr(UT))
+    return UT, rec[: len(nodes)]
+
+
+def window(prob, lo, hi, ltype, rtype, p, gL, gR, send_kind, sendL_node=-1, sendR_node=-1, rec_nodes=()):
+    """One subdomain window solve; returns (uT, sendL, sendR, rec)."""
+    g = prob.grid
+    b = _Bound(prob)
+    gL = None if gL is None else np.ascontiguousarray(gL, dtype=np.float64)
+    gR = None if gR is None else np.ascontiguousarray(gR, dtype=np.float64)
+    sendL = np.zeros((g.nt, g.nx)) if sendL_node >= 0 else None
+    sendR = np.zeros((g.nt, g.nx)) if sendR_node >= 0 else None
+    nodes = np.ascontiguousarray(rec_nodes, dtype=np.int32)
+    rec = np.zeros((max(len(nodes), 1), g.nt, g.nx))
+    uT = np.zeros((hi - lo + 1, g.nx))
+    _load().orc_window(b.ref(), lo, hi, ltype, rtype, p, _ptr(gL), _ptr(gR), KIND[send_kind] if isinstance(send_kind, str) else send_kind,
+                       sendL_node, _ptr(sendL), sendR_node, _ptr(sendR), len(nodes), _ptr(nodes), _ptr(rec), _ptr(uT))
+    return uT, sendL, sendR, rec[: len(nodes)]
+
+
+def swr(prob, kind: str, p: float, overlap: int, n_sub: int, K: int, want_traces: bool = False):
+    """Jacobi SWR; returns dict(uT, uT_sub (list of slabs), UT, err_T, err_if, traces, lo, hi)."""
+    g = prob.grid
+    b = _Bound(prob)
+    lo, hi = subdomains(g.nv, n_sub, overlap)
+    tot = int(sum((h - l + 1) for l, h in zip(lo, hi))) * g.nx
+    uT_sub = np.zeros(tot)
+    uT = np.zeros((g.nv + 1, g.nx))
+    UT = np.zeros((g.nv + 1, g.nx))
+    err_T = np.zeros(K)
+    err_if = np.zeros(K)
+    traces = np.zeros((max(2 * (n_sub - 1), 1), g.nt, g.nx)) if want_traces else None
+    rc = _load().orc_swr(b.ref(), KIND[kind], p, overlap, n_sub, K, _ptr(uT_sub), _ptr(uT), _ptr(UT),
+                         _ptr(err_T), _ptr(err_if), _ptr(traces))
+    if rc != 0:
+        raise ValueError("orc_swr rejected the arguments")
+    slabs, off = [], 0
+    for l, h in zip(lo, hi):
+        n = (h - l + 1) * g.nx
+        slabs.append(uT_sub[off:off + n].reshape(h - l + 1, g.nx))
+        off += n
+    return dict(uT=uT, uT_sub=slabs, UT=UT, err_T=err_T, err_if=err_if,
+                traces=None if traces is None else traces[: 2 * (n_sub - 1)], lo=lo, hi=hi)

@@ -1,0 +1,105 @@
+"""TEST INFRASTRUCTURE ONLY -- brute-force dense solves on tiny grids.
+
+Instead of marching step by step with a Thomas solve, these functions assemble
+the WHOLE space-time linear system of one window -- every unknown u(t_n, x_m,
+v_j), n = 1..N_t, of a subdomain at once -- from the stencil definitions of
+DESIGN.md §3 (transport P:496-516, backward-Euler centred diffusion P:480-485,
+transmission rows P:539-551 / reading R11) and solve it with a dense LU
+(``numpy.linalg.solve``).  Nothing is shared with ``kfp_oracle.c``: the
+assembly is global (one matrix for all time levels), the data come straight
+from the ``kfp_inputs`` tables, and the solve is a library routine.
+
+Only usable on tiny grids (the matrix has (N_t * N_unknown_v * N_x)^2 entries).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = ["dense_window", "dense_monodomain"]
+
+
+def dense_window(prob, lo, hi, lkind="phys", rkind="phys", p=0.0, gL=None, gR=None):
+    """Solve the space-time system of subdomain [lo, hi]; returns u [(nt+1), (hi-lo+1), nx].
+
+    lkind/rkind: 'phys' (Dirichlet 0), 'dirichlet' (value = trace), 'robin'
+    ((p -/+ d_v) u = trace with the half-cell row).  gL/gR: [nt, nx] traces
+    (row n-1 = t_n)."""
+    g = prob.grid
+    nx, nt = g.nx, g.nt
+    hx, hv, dt = 1.0 / nx, 2.0 * g.vmax / g.nv, g.t_final / nt
+    a = dt / hv ** 2
+    v = -g.vmax + np.arange(g.nv + 1) * hv
+    first = lo if lkind == "robin" else lo + 1
+    last = hi if rkind == "robin" else hi - 1
+    nu = last - first + 1
+    N = nt * nu * nx
+
+    def idx(n, j, m):  # n = 1..nt, j = first..last
+        return ((n - 1) * nu + (j - first)) * nx + (m % nx)
+
+    u0 = prob.u0_dense()
+    A = np.zeros((N, N))
+    b = np.zeros(N)
+    known = {}  # (n, j) -> row vector over m of known end values
+
+    def end_value(n, j):
+        if j < first:
+            return np.zeros(nx) if lkind == "phys" else np.asarray(gL[n - 1])
+        return np.zeros(nx) if rkind == "phys" else np.asarray(gR[n - 1])
+
+    for n in range(1, nt + 1):
+        f = prob.f_dense(n)
+        for j in range(first, last + 1):
+            nuj = v[j] * dt / hx
+            for m in range(nx):
+                row = idx(n, j, m)
+                # implicit diffusion part
+                diag = 1.0 + 2.0 * a
+                cl, cr = -a, -a
+                rhs = dt * f[j, m]
+                if j == lo and lkind == "robin":
+                    diag += 2.0 * a * p * hv
+                    cr = -2.0 * a
+                    cl = 0.0
+                    rhs += 2.0 * a * hv * gL[n - 1, m]
+                if j == hi and rkind == "robin":
+                    diag += 2.0 * a * p * hv
+                    cl = -2.0 * a
+                    cr = 0.0
+                    rhs += 2.0 * a * hv * gR[n - 1, m]
+                A[row, row] += diag
+                for jn, coef in ((j - 1, cl), (j + 1, cr)):
+                    if coef == 0.0:
+                        continue
+                    if first <= jn <= last:
+                        A[row, idx(n, jn, m)] += coef
+                    else:
+                        rhs -= coef * end_value(n, jn)[m]
+                # explicit transport of level n-1 (minus sign: moved to the left side)
+                if v[j] > 0:
+                    terms = ((m, 1.0 - nuj), (m - 1, nuj))
+                elif v[j] < 0:
+                    terms = ((m, 1.0 + nuj), (m + 1, -nuj))
+                else:
+                    terms = ((m, 1.0),)
+                for mm, coef in terms:
+                    if n == 1:
+                        rhs += coef * u0[j, mm % nx]
+                    else:
+                        A[row, idx(n - 1, j, mm)] -= coef
+                b[row] = rhs
+    x = np.linalg.solve(A, b)
+    out = np.zeros((nt + 1, hi - lo + 1, nx))
+    out[0] = u0[lo:hi + 1]
+    for n in range(1, nt + 1):
+        for j in range(lo, hi + 1):
+            if first <= j <= last:
+                out[n, j - lo] = x[idx(n, j, 0):idx(n, j, 0) + nx]
+            else:
+                out[n, j - lo] = end_value(n, j)
+    return out
+
+
+def dense_monodomain(prob):
+    """All time levels of the monodomain solution, [(nt+1), (nv+1), nx]."""
+    return dense_window(prob, 0, prob.grid.nv)
