@@ -1,0 +1,263 @@
+#!/usr/bin/env python
+"""Benchmark of the SWR hot path (BASELINE.json metric: grid-point updates/s, N_x N_v N_t K / wall).
+
+One bench "step" = one complete Jacobi SWR solve of the workload (K iterations:
+every subdomain's window of N_t fused step launches, trace exchange, error
+accumulation), inputs resident in HBM (the monodomain reference is computed
+once before timing, as SURVEY.md §8(d) prescribes).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c3|c4|c4wG|...]
+
+N = 1: workload c2 (BASELINE.json configs[2], "single-GPU large Robin SWR").
+N > 1 (torchrun, one process per GPU, NCCL): the weak-scaling c4 family
+(N_v = 4096 N, S = 4 N); configs[4] itself at N = 8.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import kfp_inputs as ki  # noqa: E402
+
+BYTES_PER_UPDATE = 16  # read u^n + write u^{n+1}, fp64
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def default_workload(n_gpus: int) -> str:
+    return "c2" if n_gpus == 1 else f"c4w{n_gpus}"
+
+
+def oracle_sample(run: ki.Run, budget_updates: float = 2.5e9):
+    """A bounded sample of the workload for the CPU oracle: the same grid (same a, CFL, dt), the
+    window cut to n_t' steps (t_final scaled so dt is unchanged) and K' = 1 iteration."""
+    g = run.grid
+    per_step = g.nx * g.nv * 2  # monodomain + one SWR iteration per step
+    nt = int(max(1, min(g.nt, budget_updates // per_step)))
+    dt = g.t_final / g.nt
+    return ki.scaled(run, nt=nt, K=1, t_final=dt * nt, name=run.name + "_sample")
+
+
+def run_cpu_oracle(run: ki.Run, steps: int = 1):
+    """Time the oracle as it stands on the host cores; returns (updates/s, cores, sample text)."""
+    import oracle
+
+    sample = oracle_sample(run)
+    prob = ki.make_problem(sample)
+    g = sample.grid
+    updates = g.nx * g.nv * g.nt * (1 + sample.K)  # monodomain window + K iterations of windows
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.swr(prob, sample.kind, sample.p, sample.overlap, sample.n_sub, sample.K)
+    dt = time.perf_counter() - t0
+    text = (f"{run.name} grid {g.nx}x{g.nv}, same dt/CFL, window cut to n_t={g.nt} steps, K=1, "
+            f"plus the monodomain window; {updates:.3g} updates per step")
+    return updates * steps / dt, oracle.num_threads(), text, dt / steps
+
+
+def bench_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    run = ki.config(args.workload or default_workload(args.gpus))
+    for _ in range(max(0, min(args.warmup, 1))):
+        run_cpu_oracle(run, 1)
+    value, cores, text, per_step = run_cpu_oracle(run, args.steps)
+    line = {
+        "impl": "reference", "metric": "grid-point updates/s (N_x*N_v*N_t*K / wall)", "value": value,
+        "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": {"workload": run.name, "oracle_sample": text},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "oracle", "sample": text},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_single(args):
+    import torch
+
+    from paper_1306_4596_b200 import Problem
+
+    run = ki.config(args.workload or default_workload(1))
+    g = run.grid
+    prob = ki.make_problem(run)
+    dev = 0
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    pb = Problem(prob, device=dev)
+    pb.set_stream(stream.cuda_stream)
+    pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)  # monodomain reference happens here (untimed)
+    torch.cuda.synchronize()
+
+    def one():
+        pb.reset()
+        pb.iterate(run.K)
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    launches0 = pb.launch_count()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_kernel_ms = 0.0
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        one()
+        # window times of this solve (events recorded by the library on the same stream)
+        _, kms = pb.last_timing()
+        step_kernel_ms += kms
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    launches = pb.launch_count() - launches0
+    updates = run.updates
+    value = updates * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (the fused step): algorithmic bytes per launch / avg duration
+    rows = sum(pb.subdomain_range(s)[1] - pb.subdomain_range(s)[0] + 1 for s in range(run.n_sub))
+    unknown_rows = rows - 2 * (run.n_sub - 1) * (0 if run.kind == "robin" else 1) - 2  # physical ends not solved
+    step_launches = g.nt * run.K * args.steps
+    per_launch_s = step_kernel_ms / 1e3 / step_launches
+    bytes_per_launch = BYTES_PER_UPDATE * g.nx * unknown_rows
+    achieved = bytes_per_launch / per_launch_s / 1e9
+    peak, peak_kind = measured_peaks()
+    eT, eI = pb.history()
+    plan = pb.plan()
+
+    # end to end through the public API with host buffers (create -> solve -> read back)
+    e2e_steps = max(1, min(args.steps, 2))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    d2h = 0
+    for _ in range(e2e_steps):
+        with Problem(prob, device=dev) as q:
+            q.set_stream(stream.cuda_stream)
+            uT = q.solve(run.kind, run.p, run.overlap, run.n_sub, run.K)
+            h = q.history()
+            d2h = uT.nbytes + h[0].nbytes + h[1].nbytes
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    e2e_value = updates / (e2e_ms / 1e3)
+
+    cpu = None
+    if not args.no_cpu:
+        v, cores, text, _ = run_cpu_oracle(run, 1)
+        cpu = {"value": v, "unit": "updates/s", "cores": cores, "kind": "oracle", "sample": text}
+
+    line = {
+        "metric": "grid-point updates/s (N_x*N_v*N_t*K / wall)", "value": value, "unit": "updates/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": run.name, "nx": g.nx, "nv": g.nv, "nt": g.nt, "K": run.K, "n_sub": run.n_sub,
+                   "kind": run.kind, "p": run.p, "overlap": run.overlap, "plan": plan,
+                   "l2": "inputs larger than L2 (two fp64 slab pairs of %.0f MB vs 126 MB L2)" %
+                         (2 * 8 * g.nx * (g.nv + run.n_sub) / 1e6),
+                   "parallelism": "v-subdomains on 1 GPU", "updates_per_step": updates},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_kind": peak_kind, "kernel": "kfp::step_fused",
+                     "bytes_per_launch": bytes_per_launch, "avg_launch_us": per_launch_s * 1e6},
+        "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": pb.h2d_bytes,
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "cpu_baseline": cpu,
+        "err_T_last": float(eT[-1]), "err_if_last": float(eI[-1]),
+    }
+    pb.close()
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return bench_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_1306_4596_b200 import dist
+
+        return dist.bench_main(args, default_workload)
+    return bench_single(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

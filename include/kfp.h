@@ -1,0 +1,187 @@
+/*
+ * kfp.h -- C-ABI of the B200 (sm_100a) Schwarz-waveform-relaxation solver for
+ * the Kolmogorov equation  u_t + v u_x - u_vv = f  (arXiv 1306.4596,
+ * PAPER.md:22-25 eq. Intro1 and P:33-38 eq. Kolmogorovmain).
+ *
+ * The solver computes, on x in [0,1) periodic (N_x nodes) and v in
+ * [-Vmax, Vmax] (N_v cells, N_v+1 nodes, homogeneous Dirichlet ends), with
+ * N_t steps of dt = T/N_t:
+ *   - one step = explicit first-order upwind transport in x (P:496-516,
+ *     weight |v_j| dt/h_x) then a backward-Euler centred diffusion solve in v,
+ *     one tridiagonal system per x-column; full dt, forcing at
+ *     t_{n+1} (readings R1-R8);
+ *   - the v-axis split into n_sub contiguous subdomains iterated
+ *     by Jacobi SWR (the Remark at P:594-597) with Dirichlet
+ *     (classical) or Robin (optimised; one-sided p = q,
+ *     P:613) transmission of whole-window traces (eq. lambda12);
+ *   - per-iteration errors of the iterates against the monodomain discrete
+ *     solution (BASELINE.json north_star (c)).
+ *
+ * Conventions (all entry points):
+ *   - every floating-point array is fp64;
+ *   - 2-D arrays are v-major: element (v-node j, x-node m) at [j*nx + m];
+ *   - pointers marked "host" are host memory owned by the caller; the library
+ *     copies inputs during the call and never keeps a host pointer;
+ *   - pointers marked "device" are CUDA device memory on the problem's device,
+ *     owned by the caller, and must stay valid while the library uses them;
+ *   - every call returns a kfp_status; on error the state of the problem is
+ *     unchanged unless stated otherwise, and kfp_last_error() returns a
+ *     thread-local human-readable message;
+ *   - a handle is used by one host thread at a time;
+ *   - work is queued on the problem's CUDA stream (kfp_set_stream); calls that
+ *     return host data synchronise that stream.
+ * There is no CPU fallback: every numerical step runs in this library's CUDA
+ * kernels; creating a problem without a usable sm_100 device returns
+ * KFP_E_CUDA.
+ */
+#ifndef KFP_H
+#define KFP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kfp_problem_s *kfp_problem; /* opaque; owns all device memory it allocates */
+
+typedef enum {
+    KFP_OK = 0,
+    KFP_E_INVAL = -1,  /* invalid argument (sizes, decomposition, p, K, ...) */
+    KFP_E_CFL = -2,    /* Vmax * dt / h_x > 1: the upwind step would not be a convex combination */
+    KFP_E_NOMEM = -3,  /* device allocation failed */
+    KFP_E_CUDA = -4,   /* CUDA runtime error or no usable device */
+    KFP_E_STATE = -6   /* call order (e.g. history before any solve) */
+} kfp_status;
+
+typedef enum {
+    KFP_DIRICHLET = 0, /* classical SWR (CSWR): Q1 = Q2 = identity */
+    KFP_ROBIN = 1      /* optimised SWR OSWR(p): Q1 = p + d_v, Q2 = p - d_v (p = q) */
+} kfp_kind;
+
+/* Problem description (PAPER.md:33-38 data f, u0, T; grid per DESIGN.md R5/R6).
+ * f(t_n, x_m, v_j) = sum_{r<f_rank} ft[r*(nt+1)+n] * fv[r*(nv+1)+j] * fx[r*nx+m]
+ * u0(x_m, v_j)     = sum_{r<u0_rank} u0v[r*(nv+1)+j] * u0x[r*nx+m]   (u0_rank = 0: u0 = 0)
+ * with x_m = m/nx, v_j = -vmax + j*2*vmax/nv, t_n = n*t_final/nt.
+ * Requirements: nx >= 2 and even, nv >= 2 and even, nt >= 1, vmax > 0,
+ * t_final > 0, 0 <= f_rank <= 4, 0 <= u0_rank <= 4; tables are host memory. */
+typedef struct {
+    int32_t nx, nv, nt;
+    double vmax, t_final;
+    int32_t f_rank;
+    const double *ft, *fv, *fx; /* host */
+    int32_t u0_rank;
+    const double *u0v, *u0x;    /* host */
+    int32_t device;             /* CUDA device ordinal */
+} kfp_problem_desc;
+
+/* Validate the description, select the device, copy the tables to device
+ * memory and create the problem's stream.  KFP_E_INVAL for bad sizes/ranks,
+ * KFP_E_CFL if vmax*(t_final/nt)*nx > 1, KFP_E_CUDA if the device is unusable.
+ * *out is set only on success. */
+kfp_status kfp_problem_create(const kfp_problem_desc *desc, kfp_problem *out);
+
+/* Free every device buffer and the handle (NULL is a no-op). */
+void kfp_problem_destroy(kfp_problem pb);
+
+/* Run all subsequent work on `stream` (a cudaStream_t on the problem's
+ * device, e.g. torch.cuda.current_stream().cuda_stream); NULL restores the
+ * problem's own stream. */
+kfp_status kfp_set_stream(kfp_problem pb, void *stream);
+
+/* Monodomain solve (the SWR reference, BJ north_star (c)): the same scheme on
+ * nodes [0, nv] with physical Dirichlet ends.  uT: host [(nv+1)*nx] receiving
+ * U(T), or NULL to keep it on the device only. */
+kfp_status kfp_monodomain_solve(kfp_problem pb, double *uT);
+
+/* Configure a Jacobi SWR solve and allocate its buffers.
+ *  kind     : KFP_DIRICHLET or KFP_ROBIN;  p > 0 required for KFP_ROBIN.
+ *  overlap  : overlap in v-cells; subdomain s covers nodes [lo_s, hi_s] with
+ *             c_s = s*nv/n_sub, lo_0 = 0, lo_s = c_s - floor(overlap/2),
+ *             hi_s = c_{s+1} + ceil(overlap/2), hi_{n_sub-1} = nv (R9).
+ *  n_sub    : number of subdomains, nv % n_sub == 0, 0 <= overlap < nv/n_sub - 2.
+ *  s_begin, s_end : the contiguous block [s_begin, s_end) of subdomains this
+ *             process solves (0, n_sub for a single process); traces across the
+ *             block's edges are exchanged by the caller (kfp_swr_edge_buffers).
+ *  K_max    : capacity of the error history (K_max >= 1).
+ * Runs the monodomain reference if it has not been run for the interface
+ * lines this decomposition needs.  Dirichlet with overlap 0 is accepted (it
+ * does not converge) and sets a warning in kfp_last_error(). */
+kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overlap, int32_t n_sub,
+                         int32_t s_begin, int32_t s_end, int32_t K_max);
+
+/* Reset to iteration 0: zero incoming traces (the initial guess) and
+ * clear the error history. */
+kfp_status kfp_swr_reset(kfp_problem pb);
+
+/* Run n_iter Jacobi iterations on the local block (each: every local
+ * subdomain solves the whole window [0,T] from u0 with the previous
+ * iteration's traces, writes its outgoing traces and accumulates its errors;
+ * local interfaces are exchanged on the device).  Asynchronous on the
+ * problem's stream.  KFP_E_STATE if more than K_max iterations in total. */
+kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter);
+
+/* Device pointers of the cross-block exchange buffers, each [nt][nx] fp64
+ * (row n-1 = value at t_n), for the parity iteration `k & 1` that the NEXT
+ * kfp_swr_iterate call reads: after iteration k the caller must copy the left
+ * neighbour block's send_right into recv_left and the right neighbour's
+ * send_left into recv_right (NCCL send/recv).  Pointers are NULL where the
+ * block touches a physical end.  Parity: buffers written by iteration k are
+ * send_*[k & 1]; buffers read by iteration k+1 are recv_*[k & 1]. */
+kfp_status kfp_swr_edge_buffers(kfp_problem pb, int32_t parity, double **send_left, double **recv_left,
+                                double **send_right, double **recv_right);
+
+/* Replace the library's cross-block exchange buffers of iteration parity
+ * `parity` with caller-owned device buffers (e.g. torch tensors that NCCL
+ * send/recv use directly), each [nt][nx] fp64; NULL keeps the current buffer.
+ * Buffers for a side the block does not have must be NULL.  recv buffers of
+ * parity 0 are zeroed by kfp_swr_reset (the zero initial guess). */
+kfp_status kfp_swr_bind_edge_buffers(kfp_problem pb, int32_t parity, double *send_left, double *recv_left,
+                                     double *send_right, double *recv_right);
+
+/* Convenience: setup(s_begin=0, s_end=n_sub, K_max=K) + reset + iterate(K) on
+ * one process.  uT: host [(nv+1)*nx] receiving u^K(T) assembled by nominal
+ * ownership (node j from the subdomain s with c_s <= j < c_{s+1}, node nv from
+ * n_sub-1), or NULL. */
+kfp_status kfp_swr_solve(kfp_problem pb, kfp_kind kind, double p, int32_t overlap, int32_t n_sub, int32_t K,
+                         double *uT);
+
+/* Error history of the iterations run since the last reset, from the local
+ * block: err_T[k-1] = max_{s,m, j in [lo_s,hi_s]} |u_s^k(T) - U(T)|,
+ * err_if[k-1] = max over s, its interface end nodes (lo_s for s>0, hi_s for
+ * s<n_sub-1), n = 1..nt and m of |u_s^k(t_n) - U(t_n)|.  Host arrays of
+ * length cap; *K_out = number of iterations run.  KFP_E_STATE before any
+ * iteration. */
+kfp_status kfp_error_history(kfp_problem pb, int32_t cap, int32_t *K_out, double *err_T, double *err_if);
+
+/* Copy the local subdomain s's current u_s(T) slab [(hi_s-lo_s+1)*nx] to host
+ * memory (s is the global subdomain index, s_begin <= s < s_end). */
+kfp_status kfp_swr_subdomain_uT(kfp_problem pb, int32_t s, double *out);
+
+/* Node range of global subdomain s under the current setup. */
+kfp_status kfp_swr_subdomain_range(kfp_problem pb, int32_t s, int32_t *lo, int32_t *hi);
+
+/* Copy the most recent outgoing trace of interface i (between subdomains i and
+ * i+1; both must be local) to host memory [nt*nx]: dir 0 = sent leftwards by
+ * i+1 (used at hi_i), dir 1 = sent rightwards by i (used at lo_{i+1}). */
+kfp_status kfp_swr_trace(kfp_problem pb, int32_t i, int32_t dir, double *out);
+
+/* Copy the monodomain U(T) [(nv+1)*nx] to host memory. */
+kfp_status kfp_monodomain_uT(kfp_problem pb, double *out);
+
+/* Number of this library's kernels launched since creation (for the bench's
+ * gpu_launches claim) and a short description of the selected launch plan. */
+int64_t kfp_launch_count(kfp_problem pb);
+const char *kfp_plan(kfp_problem pb);
+
+/* Device time in milliseconds of the most recent kfp_swr_iterate call and of
+ * the step kernels inside it, measured with CUDA events on the problem's
+ * stream (synchronises).  *kernel_ms may be NULL. */
+kfp_status kfp_last_timing(kfp_problem pb, double *iterate_ms, double *kernel_ms);
+
+const char *kfp_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KFP_H */

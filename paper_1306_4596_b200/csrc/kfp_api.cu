@@ -1,0 +1,921 @@
+// kfp_api.cu -- host side of the C-ABI declared in include/kfp.h.
+//
+// Owns the device memory of one problem, validates arguments, precomputes the
+// O(N_v + N_x) constant tables (transport weights, powers of q, Woodbury 2x2
+// inverses per subdomain), plans the launch geometry and drives the Jacobi
+// SWR iteration as a sequence of step launches on one
+// CUDA stream.  Every numerical step of the path runs in kfp_device.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kfp.h"
+#include "kfp_device.cuh"
+
+using kfp::SubDev;
+using kfp::StepParams;
+
+namespace {
+thread_local std::string g_err;
+
+void set_err(const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+#define KFP_CUDA(call)                                                                         \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            set_err("CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__, __LINE__,    \
+                    cudaGetErrorString(e_));                                                   \
+            return e_ == cudaErrorMemoryAllocation ? KFP_E_NOMEM : KFP_E_CUDA;                 \
+        }                                                                                      \
+    } while (0)
+
+struct Plan {
+    bool fused = false;
+    int P = 8, b = 32, R = 256, C = 1;
+    size_t smem = 0;
+    std::string text;
+};
+
+// Launch geometry for columns of at most n_max unknown rows:
+// P = 8 warps per CTA, chunks of b rows, row blocks of R = P b rows; C blocks
+// per column.  C <= 8 -> one thread-block cluster per 32-column tile (fused
+// kernel); otherwise the three-phase path with global block aggregates.
+Plan make_plan(int n_max, bool allow_fused) {
+    Plan pl;
+    pl.P = 8;
+    const int target = 256;
+    int C = (n_max + target - 1) / target;
+    if (allow_fused && C <= 8) {
+        pl.fused = true;
+        pl.C = std::max(1, C);
+        pl.b = (n_max + pl.C * pl.P - 1) / (pl.C * pl.P);
+        pl.b = std::max(pl.b, 2);
+    } else {
+        pl.fused = false;
+        pl.b = 32;
+        pl.C = (n_max + pl.P * pl.b - 1) / (pl.P * pl.b);
+    }
+    pl.R = pl.P * pl.b;
+    pl.smem = kfp::smem_bytes(pl.R, pl.P);
+    char buf[160];
+    snprintf(buf, sizeof buf, "%s P=%d b=%d R=%d C=%d smem=%zu", pl.fused ? "fused-cluster" : "three-phase", pl.P,
+             pl.b, pl.R, pl.C, pl.smem);
+    pl.text = buf;
+    return pl;
+}
+}  // namespace
+
+struct kfp_problem_s {
+    int device = 0;
+    cudaStream_t own_stream = nullptr, stream = nullptr;
+    int nx = 0, nv = 0, nt = 0;
+    double vmax = 0, T = 0, hx = 0, hv = 0, dt = 0, a = 0, q = 0;
+    int f_rank = 0, u0_rank = 0;
+    std::vector<double> ft;  // host [f_rank][nt+1]
+    double *d_fv = nullptr, *d_fx = nullptr, *d_u0v = nullptr, *d_u0x = nullptr;
+    double2 *d_rowc = nullptr;
+    double *d_qp = nullptr, *d_s2 = nullptr;
+    int qtab_len = 0;
+    std::vector<void *> allocs;  // everything else (freed at destroy)
+
+    // monodomain
+    bool mono_done = false;
+    std::vector<int> mono_lines;  // node list recorded in d_Ulines
+    double *d_mono[2] = {nullptr, nullptr};
+    double *d_UT = nullptr;
+    double *d_Ulines = nullptr;
+    int *d_line_of_node = nullptr;
+
+    // SWR
+    bool setup = false;
+    int kind = 0;
+    double p = 0;
+    int ov = 0, S = 0, s_begin = 0, s_end = 0, K_max = 0, k_done = 0;
+    std::vector<int> lo, hi;
+    std::vector<SubDev> subs;  // local block
+    SubDev *d_subs = nullptr;
+    unsigned long long *d_errT = nullptr, *d_errIF = nullptr;
+    Plan plan;
+    double *d_blkagg = nullptr, *d_chkagg = nullptr, *d_carry = nullptr;
+    std::vector<double *> swr_allocs;
+    double *edge_sendL[2] = {nullptr, nullptr}, *edge_recvL[2] = {nullptr, nullptr};
+    double *edge_sendR[2] = {nullptr, nullptr}, *edge_recvR[2] = {nullptr, nullptr};
+    std::vector<double *> zero_on_reset;  // parity-0 incoming buffers
+
+    int64_t launches = 0;
+    std::vector<cudaEvent_t> ev;  // 2 per iteration of the last iterate call + 2 around it
+    int ev_used = 0;
+    std::string plan_text;
+};
+
+namespace {
+
+template <class T>
+kfp_status dalloc(kfp_problem pb, T **p, size_t count, std::vector<void *> *list = nullptr) {
+    void *q = nullptr;
+    KFP_CUDA(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T)));
+    *p = static_cast<T *>(q);
+    (list ? *list : pb->allocs).push_back(q);
+    return KFP_OK;
+}
+
+void free_swr(kfp_problem pb) {
+    for (double *p : pb->swr_allocs) cudaFree(p);
+    pb->swr_allocs.clear();
+    pb->subs.clear();
+    pb->zero_on_reset.clear();
+    if (pb->d_subs) cudaFree(pb->d_subs);
+    pb->d_subs = nullptr;
+    if (pb->d_errT) cudaFree(pb->d_errT);
+    if (pb->d_errIF) cudaFree(pb->d_errIF);
+    pb->d_errT = pb->d_errIF = nullptr;
+    pb->d_blkagg = pb->d_chkagg = pb->d_carry = nullptr;
+    for (int q = 0; q < 2; ++q) pb->edge_sendL[q] = pb->edge_recvL[q] = pb->edge_sendR[q] = pb->edge_recvR[q] = nullptr;
+    pb->setup = false;
+}
+
+kfp_status swr_alloc(kfp_problem pb, double **p, size_t count) {
+    void *q = nullptr;
+    KFP_CUDA(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(double)));
+    *p = static_cast<double *>(q);
+    pb->swr_allocs.push_back(*p);
+    return KFP_OK;
+}
+
+// Subdomain node ranges (R9).
+void decompose(int nv, int S, int ov, std::vector<int> &lo, std::vector<int> &hi) {
+    lo.assign(S, 0);
+    hi.assign(S, 0);
+    for (int s = 0; s < S; ++s) {
+        const int cs = s * (nv / S), cs1 = (s + 1) * (nv / S);
+        lo[s] = (s == 0) ? 0 : cs - ov / 2;
+        hi[s] = (s == S - 1) ? nv : cs1 + (ov + 1) / 2;
+    }
+}
+
+// Woodbury constants of one column system.
+void woodbury(const kfp_problem pb, SubDev &sd, double p) {
+    const long double a = pb->a, q = pb->q, h = pb->hv;
+    const int n = sd.n;
+    // d_t on rows (0,1), d_b on rows (n-2, n-1)
+    long double wt0, wt1, wb0, wb1;
+    if (sd.ltype == kfp::END_ROBIN) {
+        wt0 = a * (2.0L * p * h + q);
+        wt1 = -a;
+    } else {
+        wt0 = a * q;
+        wt1 = 0.0L;
+    }
+    if (sd.rtype == kfp::END_ROBIN) {
+        wb0 = -a;
+        wb1 = 2.0L * a * p * h;
+    } else {
+        wb0 = 0.0L;
+        wb1 = 0.0L;
+    }
+    // z0 = B^{-1} e_0, z1 = B^{-1} e_{n-1}: forward y_i = q y_{i-1} + (q/a) e_i, backward x_i = q x_{i+1} + y_i.
+    auto solveB = [&](int unit, long double out[4]) {
+        std::vector<long double> y(n), x(n + 1, 0.0L);
+        long double prev = 0.0L;
+        for (int i = 0; i < n; ++i) {
+            prev = q * prev + ((i == unit) ? q / a : 0.0L);
+            y[i] = prev;
+        }
+        for (int i = n - 1; i >= 0; --i) x[i] = q * x[i + 1] + y[i];
+        const int rows[4] = {0, 1, n - 2, n - 1};
+        for (int k = 0; k < 4; ++k) out[k] = (rows[k] >= 0 && rows[k] < n) ? x[rows[k]] : 0.0L;
+    };
+    long double z0[4], z1[4];
+    solveB(0, z0);
+    solveB(n - 1, z1);
+    const long double M00 = 1.0L + wt0 * z0[0] + wt1 * z0[1];
+    const long double M01 = wt0 * z1[0] + wt1 * z1[1];
+    const long double M10 = wb0 * z0[2] + wb1 * z0[3];
+    const long double M11 = 1.0L + wb0 * z1[2] + wb1 * z1[3];
+    const long double det = M00 * M11 - M01 * M10;
+    sd.wt0 = (double)wt0;
+    sd.wt1 = (double)wt1;
+    sd.wb0 = (double)wb0;
+    sd.wb1 = (double)wb1;
+    sd.Mi00 = (double)(M11 / det);
+    sd.Mi01 = (double)(-M01 / det);
+    sd.Mi10 = (double)(-M10 / det);
+    sd.Mi11 = (double)(M00 / det);
+}
+
+kfp_status ensure_qtab(kfp_problem pb, int len) {
+    if (len <= pb->qtab_len) return KFP_OK;
+    std::vector<double> qp(len), s2(len);
+    long double qq = 1.0L, ss = 0.0L;
+    const long double q = pb->q;
+    for (int k = 0; k < len; ++k) {
+        qp[k] = (double)qq;
+        s2[k] = (double)ss;  // sum_{t<k} q^{2t}
+        ss += qq * qq;
+        qq *= q;
+    }
+    double *dq = nullptr, *ds = nullptr;
+    if (kfp_status st = dalloc(pb, &dq, len)) return st;
+    if (kfp_status st = dalloc(pb, &ds, len)) return st;
+    KFP_CUDA(cudaMemcpy(dq, qp.data(), len * sizeof(double), cudaMemcpyHostToDevice));
+    KFP_CUDA(cudaMemcpy(ds, s2.data(), len * sizeof(double), cudaMemcpyHostToDevice));
+    pb->d_qp = dq;
+    pb->d_s2 = ds;
+    pb->qtab_len = len;
+    return KFP_OK;
+}
+
+StepParams base_params(kfp_problem pb) {
+    StepParams P;
+    std::memset(&P, 0, sizeof P);
+    P.nx = pb->nx;
+    P.nv = pb->nv;
+    P.nt = pb->nt;
+    P.f_rank = pb->f_rank;
+    P.u0_rank = pb->u0_rank;
+    P.q = pb->q;
+    P.a = pb->a;
+    P.qa = pb->q / pb->a;
+    P.hv = pb->hv;
+    P.dt = pb->dt;
+    P.rowc = pb->d_rowc;
+    P.fv = pb->d_fv;
+    P.fx = pb->d_fx;
+    P.u0v = pb->d_u0v;
+    P.u0x = pb->d_u0x;
+    P.qp = pb->d_qp;
+    P.s2 = pb->d_s2;
+    P.qtab_len = pb->qtab_len;
+    return P;
+}
+
+// One time step of every subdomain in `subs` (device array of nsub entries).
+kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, int n) {
+    P.n = n;
+    P.from_u0 = (n == 0);
+    for (int r = 0; r < kfp::kMaxRank; ++r) P.cf[r] = (r < pb->f_rank) ? pb->dt * pb->ft[(size_t)r * (pb->nt + 1) + n + 1] : 0.0;
+    P.P = pl.P;
+    P.b = pl.b;
+    P.R = pl.R;
+    P.C = pl.C;
+    const int ntiles = (pb->nx + kfp::kWarp - 1) / kfp::kWarp;
+    const dim3 block(pl.P * kfp::kWarp);
+    if (pl.fused) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(pl.C, ntiles, nsub);
+        cfg.blockDim = block;
+        cfg.dynamicSmemBytes = pl.smem;
+        cfg.stream = pb->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = pl.C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        KFP_CUDA(cudaLaunchKernelEx(&cfg, kfp::step_fused, P));
+        pb->launches += 1;
+    } else {
+        kfp::step_phase1<<<dim3(pl.C, ntiles, nsub), block, pl.smem, pb->stream>>>(P);
+        kfp::step_phase2<<<dim3((pb->nx + 127) / 128, 1, nsub), 128, 0, pb->stream>>>(P);
+        kfp::step_phase3<<<dim3(pl.C, ntiles, nsub), block, pl.smem, pb->stream>>>(P);
+        pb->launches += 3;
+    }
+    KFP_CUDA(cudaGetLastError());
+    return KFP_OK;
+}
+
+kfp_status configure_kernels(const Plan &pl) {
+    if (pl.fused) {
+        KFP_CUDA(cudaFuncSetAttribute(kfp::step_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        if (pl.C > 8) KFP_CUDA(cudaFuncSetAttribute(kfp::step_fused, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    } else {
+        KFP_CUDA(cudaFuncSetAttribute(kfp::step_phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        KFP_CUDA(cudaFuncSetAttribute(kfp::step_phase3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    }
+    return KFP_OK;
+}
+
+kfp_status alloc_general_scratch(kfp_problem pb, const Plan &pl, int nsub, double **blkagg, double **chkagg,
+                                 double **carry, std::vector<double *> &owner) {
+    const size_t nx = pb->nx;
+    auto al = [&](double **p, size_t c) -> kfp_status {
+        void *q = nullptr;
+        KFP_CUDA(cudaMalloc(&q, std::max<size_t>(c, 1) * sizeof(double)));
+        *p = static_cast<double *>(q);
+        owner.push_back(*p);
+        return KFP_OK;
+    };
+    if (pl.fused) {
+        *blkagg = *chkagg = *carry = nullptr;
+        return KFP_OK;
+    }
+    if (kfp_status st = al(blkagg, (size_t)nsub * pl.C * 8 * nx)) return st;
+    if (kfp_status st = al(chkagg, (size_t)nsub * pl.C * pl.P * 2 * nx)) return st;
+    if (kfp_status st = al(carry, (size_t)nsub * pl.C * 2 * nx)) return st;
+    KFP_CUDA(cudaMemset(*blkagg, 0, (size_t)nsub * pl.C * 8 * nx * sizeof(double)));
+    return KFP_OK;
+}
+
+// Monodomain solve recording U at `lines` (BJ north_star (c)).
+kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
+    const size_t nx = pb->nx, nn = (size_t)pb->nv + 1;
+    if (!pb->d_mono[0]) {
+        for (int q = 0; q < 2; ++q)
+            if (kfp_status st = dalloc(pb, &pb->d_mono[q], nn * nx)) return st;
+        if (kfp_status st = dalloc(pb, &pb->d_line_of_node, nn)) return st;
+    }
+    for (int q = 0; q < 2; ++q) KFP_CUDA(cudaMemsetAsync(pb->d_mono[q], 0, nn * nx * sizeof(double), pb->stream));
+    std::vector<int> lon(nn, -1);
+    for (size_t i = 0; i < lines.size(); ++i) lon[lines[i]] = (int)i;
+    KFP_CUDA(cudaMemcpyAsync(pb->d_line_of_node, lon.data(), nn * sizeof(int), cudaMemcpyHostToDevice, pb->stream));
+    if (pb->d_Ulines) {
+        cudaFree(pb->d_Ulines);
+        pb->allocs.erase(std::find(pb->allocs.begin(), pb->allocs.end(), (void *)pb->d_Ulines));
+        pb->d_Ulines = nullptr;
+    }
+    if (!lines.empty())
+        if (kfp_status st = dalloc(pb, &pb->d_Ulines, lines.size() * (size_t)pb->nt * nx)) return st;
+
+    SubDev sd;
+    std::memset(&sd, 0, sizeof sd);
+    sd.lo = 0;
+    sd.hi = pb->nv;
+    sd.first = 1;
+    sd.n = pb->nv - 1;
+    sd.ltype = sd.rtype = kfp::END_PHYS;
+    sd.iL_tr = sd.iR_tr = -2;
+    sd.ifL = sd.ifR = -1;
+    sd.slab[0] = pb->d_mono[0];
+    sd.slab[1] = pb->d_mono[1];
+    woodbury(pb, sd, 0.0);
+    Plan pl = make_plan(sd.n, true);
+    sd.nblk = (sd.n + pl.R - 1) / pl.R;
+    if (kfp_status st = ensure_qtab(pb, pl.R + 2)) return st;
+    if (kfp_status st = configure_kernels(pl)) return st;
+    SubDev *d_sd = nullptr;
+    std::vector<double *> tmp;
+    KFP_CUDA(cudaMalloc(&d_sd, sizeof(SubDev)));
+    KFP_CUDA(cudaMemcpyAsync(d_sd, &sd, sizeof sd, cudaMemcpyHostToDevice, pb->stream));
+    StepParams P = base_params(pb);
+    P.subs = d_sd;
+    P.record = lines.empty() ? 0 : 1;
+    P.line_of_node = pb->d_line_of_node;
+    P.rec = pb->d_Ulines;
+    P.last = 0;  // no error accumulation on the reference itself; end rows stay 0 (memset)
+    kfp_status st = alloc_general_scratch(pb, pl, 1, &P.blkagg, &P.chkagg, &P.carry, tmp);
+    for (int n = 0; st == KFP_OK && n < pb->nt; ++n) st = launch_step(pb, pl, P, 1, n);
+    cudaError_t e = cudaStreamSynchronize(pb->stream);
+    cudaFree(d_sd);
+    for (double *q : tmp) cudaFree(q);
+    if (st != KFP_OK) return st;
+    KFP_CUDA(e);
+    pb->d_UT = pb->d_mono[pb->nt & 1];
+    pb->mono_lines = lines;
+    pb->mono_done = true;
+    return KFP_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+const char *kfp_last_error(void) { return g_err.c_str(); }
+
+kfp_status kfp_problem_create(const kfp_problem_desc *d, kfp_problem *out) {
+    if (!d || !out) {
+        set_err("kfp_problem_create: NULL argument");
+        return KFP_E_INVAL;
+    }
+    if (d->nx < 2 || d->nx % 2 || d->nv < 2 || d->nv % 2 || d->nt < 1 || !(d->vmax > 0) || !(d->t_final > 0) ||
+        d->f_rank < 0 || d->f_rank > kfp::kMaxRank || d->u0_rank < 0 || d->u0_rank > kfp::kMaxRank) {
+        set_err("kfp_problem_create: invalid sizes (nx=%d nv=%d nt=%d vmax=%g T=%g f_rank=%d u0_rank=%d); "
+                "need nx,nv >= 2 even, nt >= 1, vmax,T > 0, ranks in [0,%d]",
+                d->nx, d->nv, d->nt, d->vmax, d->t_final, d->f_rank, d->u0_rank, kfp::kMaxRank);
+        return KFP_E_INVAL;
+    }
+    if ((d->f_rank > 0 && (!d->ft || !d->fv || !d->fx)) || (d->u0_rank > 0 && (!d->u0v || !d->u0x))) {
+        set_err("kfp_problem_create: missing table pointer");
+        return KFP_E_INVAL;
+    }
+    const double hx = 1.0 / d->nx, dt = d->t_final / d->nt;
+    const double cfl = d->vmax * dt / hx;
+    if (cfl > 1.0) {
+        set_err("kfp_problem_create: CFL Vmax*dt/h_x = %.6g > 1 (upwind step not a convex combination)", cfl);
+        return KFP_E_CFL;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        set_err("kfp_problem_create: no CUDA device available (this library has no CPU path)");
+        return KFP_E_CUDA;
+    }
+    if (d->device < 0 || d->device >= ndev) {
+        set_err("kfp_problem_create: device %d out of range (%d devices)", d->device, ndev);
+        return KFP_E_INVAL;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, d->device) != cudaSuccess || prop.major < 10) {
+        set_err("kfp_problem_create: device %d is not sm_100 (compute capability %d.%d)", d->device, prop.major,
+                prop.minor);
+        return KFP_E_CUDA;
+    }
+    kfp_problem pb = new kfp_problem_s();
+    pb->device = d->device;
+    if (cudaSetDevice(d->device) != cudaSuccess || cudaStreamCreateWithFlags(&pb->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        set_err("kfp_problem_create: cannot set device / create stream");
+        delete pb;
+        return KFP_E_CUDA;
+    }
+    pb->stream = pb->own_stream;
+    pb->nx = d->nx;
+    pb->nv = d->nv;
+    pb->nt = d->nt;
+    pb->vmax = d->vmax;
+    pb->T = d->t_final;
+    pb->hx = hx;
+    pb->hv = 2.0 * d->vmax / d->nv;
+    pb->dt = dt;
+    pb->a = dt / (pb->hv * pb->hv);
+    pb->q = ((1.0 + 2.0 * pb->a) - std::sqrt(1.0 + 4.0 * pb->a)) / (2.0 * pb->a);
+    pb->f_rank = d->f_rank;
+    pb->u0_rank = d->u0_rank;
+    pb->ft.assign(d->ft, d->ft + (size_t)d->f_rank * (d->nt + 1));
+    const size_t nn = (size_t)d->nv + 1;
+    std::vector<double2> rowc(nn);
+    for (size_t j = 0; j < nn; ++j) {
+        const double v = -d->vmax + (double)j * pb->hv;
+        const double nu = std::fabs(v * dt / hx);
+        rowc[j] = make_double2(1.0 - nu, nu);
+    }
+    kfp_status st = KFP_OK;
+    auto up = [&](double **dst, const double *src, size_t cnt) -> kfp_status {
+        if (kfp_status s2 = dalloc(pb, dst, cnt)) return s2;
+        if (cnt) KFP_CUDA(cudaMemcpy(*dst, src, cnt * sizeof(double), cudaMemcpyHostToDevice));
+        return KFP_OK;
+    };
+    if (!st) st = up(&pb->d_fv, d->fv, (size_t)d->f_rank * nn);
+    if (!st) st = up(&pb->d_fx, d->fx, (size_t)d->f_rank * d->nx);
+    if (!st) st = up(&pb->d_u0v, d->u0v, (size_t)d->u0_rank * nn);
+    if (!st) st = up(&pb->d_u0x, d->u0x, (size_t)d->u0_rank * d->nx);
+    if (!st) st = up(reinterpret_cast<double **>(&pb->d_rowc), reinterpret_cast<const double *>(rowc.data()), 2 * nn);
+    if (st) {
+        kfp_problem_destroy(pb);
+        return st;
+    }
+    *out = pb;
+    return KFP_OK;
+}
+
+void kfp_problem_destroy(kfp_problem pb) {
+    if (!pb) return;
+    cudaSetDevice(pb->device);
+    if (pb->stream) cudaStreamSynchronize(pb->stream);
+    free_swr(pb);
+    for (void *p : pb->allocs) cudaFree(p);
+    for (cudaEvent_t e : pb->ev) cudaEventDestroy(e);
+    if (pb->own_stream) cudaStreamDestroy(pb->own_stream);
+    delete pb;
+}
+
+kfp_status kfp_set_stream(kfp_problem pb, void *stream) {
+    if (!pb) {
+        set_err("kfp_set_stream: NULL problem");
+        return KFP_E_INVAL;
+    }
+    pb->stream = stream ? static_cast<cudaStream_t>(stream) : pb->own_stream;
+    return KFP_OK;
+}
+
+kfp_status kfp_monodomain_solve(kfp_problem pb, double *uT) {
+    if (!pb) {
+        set_err("kfp_monodomain_solve: NULL problem");
+        return KFP_E_INVAL;
+    }
+    KFP_CUDA(cudaSetDevice(pb->device));
+    if (!pb->mono_done)
+        if (kfp_status st = run_monodomain(pb, pb->mono_lines)) return st;
+    if (uT) {
+        KFP_CUDA(cudaMemcpyAsync(uT, pb->d_UT, sizeof(double) * ((size_t)pb->nv + 1) * pb->nx, cudaMemcpyDeviceToHost,
+                                 pb->stream));
+        KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    }
+    return KFP_OK;
+}
+
+kfp_status kfp_monodomain_uT(kfp_problem pb, double *out) {
+    if (!pb || !out) {
+        set_err("kfp_monodomain_uT: NULL argument");
+        return KFP_E_INVAL;
+    }
+    if (!pb->mono_done) {
+        set_err("kfp_monodomain_uT: no monodomain solve yet");
+        return KFP_E_STATE;
+    }
+    return kfp_monodomain_solve(pb, out);
+}
+
+kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overlap, int32_t n_sub, int32_t s_begin,
+                         int32_t s_end, int32_t K_max) {
+    if (!pb) {
+        set_err("kfp_swr_setup: NULL problem");
+        return KFP_E_INVAL;
+    }
+    if (kind != KFP_DIRICHLET && kind != KFP_ROBIN) {
+        set_err("kfp_swr_setup: unknown kind %d", (int)kind);
+        return KFP_E_INVAL;
+    }
+    if (kind == KFP_ROBIN && !(p > 0)) {
+        set_err("kfp_swr_setup: Robin parameter p must be > 0 (P:58), got %g", p);
+        return KFP_E_INVAL;
+    }
+    if (n_sub < 1 || pb->nv % n_sub != 0) {
+        set_err("kfp_swr_setup: n_sub=%d must divide nv=%d", n_sub, pb->nv);
+        return KFP_E_INVAL;
+    }
+    const int cells = pb->nv / n_sub;
+    if (overlap < 0 || (n_sub > 1 && overlap >= cells - 2)) {
+        set_err("kfp_swr_setup: overlap=%d must satisfy 0 <= overlap < nv/n_sub - 2 = %d", overlap, cells - 2);
+        return KFP_E_INVAL;
+    }
+    if (s_begin < 0 || s_end > n_sub || s_begin >= s_end) {
+        set_err("kfp_swr_setup: bad local block [%d,%d) of %d subdomains", s_begin, s_end, n_sub);
+        return KFP_E_INVAL;
+    }
+    if (K_max < 1) {
+        set_err("kfp_swr_setup: K_max must be >= 1 (SPEC S:214)");
+        return KFP_E_INVAL;
+    }
+    KFP_CUDA(cudaSetDevice(pb->device));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    free_swr(pb);
+    std::string warn;
+    if (kind == KFP_DIRICHLET && overlap == 0 && n_sub > 1)
+        warn = "warning: Dirichlet transmission without overlap does not converge (P:661)";
+
+    pb->kind = kind;
+    pb->p = p;
+    pb->ov = overlap;
+    pb->S = n_sub;
+    pb->s_begin = s_begin;
+    pb->s_end = s_end;
+    pb->K_max = K_max;
+    pb->k_done = 0;
+    decompose(pb->nv, n_sub, overlap, pb->lo, pb->hi);
+
+    // interface lines needed by the local block
+    std::vector<int> lines;
+    for (int s = s_begin; s < s_end; ++s) {
+        if (s > 0) lines.push_back(pb->lo[s]);
+        if (s < n_sub - 1) lines.push_back(pb->hi[s]);
+    }
+    std::sort(lines.begin(), lines.end());
+    lines.erase(std::unique(lines.begin(), lines.end()), lines.end());
+    bool have = pb->mono_done;
+    for (int l : lines)
+        if (std::find(pb->mono_lines.begin(), pb->mono_lines.end(), l) == pb->mono_lines.end()) have = false;
+    if (!have) {
+        std::vector<int> all = pb->mono_lines;
+        all.insert(all.end(), lines.begin(), lines.end());
+        std::sort(all.begin(), all.end());
+        all.erase(std::unique(all.begin(), all.end()), all.end());
+        if (kfp_status st = run_monodomain(pb, all)) return st;
+    }
+    auto line_index = [&](int node) {
+        auto it = std::find(pb->mono_lines.begin(), pb->mono_lines.end(), node);
+        return (int)(it - pb->mono_lines.begin());
+    };
+
+    const int et = (kind == KFP_ROBIN) ? kfp::END_ROBIN : kfp::END_DIRI;
+    const int nloc = s_end - s_begin;
+    const size_t nx = pb->nx, TR = (size_t)pb->nt * nx;
+    int n_max = 0;
+    pb->subs.resize(nloc);
+    for (int i = 0; i < nloc; ++i) {
+        const int s = s_begin + i;
+        SubDev &sd = pb->subs[i];
+        std::memset(&sd, 0, sizeof sd);
+        sd.lo = pb->lo[s];
+        sd.hi = pb->hi[s];
+        sd.ltype = (s == 0) ? kfp::END_PHYS : et;
+        sd.rtype = (s == n_sub - 1) ? kfp::END_PHYS : et;
+        sd.first = (sd.ltype == kfp::END_ROBIN) ? sd.lo : sd.lo + 1;
+        const int last = (sd.rtype == kfp::END_ROBIN) ? sd.hi : sd.hi - 1;
+        sd.n = last - sd.first + 1;
+        // unknown-row index of the node whose trace is sent left / right; -2 = none.
+        // Dirichlet without overlap sends its own end node (index -1 / n): the received value.
+        sd.iL_tr = (s > 0) ? pb->hi[s - 1] - sd.first : -2;
+        sd.iR_tr = (s < n_sub - 1) ? pb->lo[s + 1] - sd.first : -2;
+        sd.ifL = (s > 0) ? line_index(sd.lo) : -1;
+        sd.ifR = (s < n_sub - 1) ? line_index(sd.hi) : -1;
+        sd.injL = (sd.ltype == kfp::END_ROBIN) ? 2.0 * pb->a * pb->hv : pb->a;
+        sd.injR = (sd.rtype == kfp::END_ROBIN) ? 2.0 * pb->a * pb->hv : pb->a;
+        if (sd.n < 2) {
+            set_err("kfp_swr_setup: subdomain %d has %d unknown rows (need >= 2)", s, sd.n);
+            return KFP_E_INVAL;
+        }
+        woodbury(pb, sd, p);
+        n_max = std::max(n_max, sd.n);
+    }
+    pb->plan = make_plan(n_max, true);
+    const Plan &pl = pb->plan;
+    // the rows of each outgoing trace stencil must sit in one row block
+    for (int i = 0; i < nloc; ++i) {
+        SubDev &sd = pb->subs[i];
+        sd.nblk = (sd.n + pl.R - 1) / pl.R;
+        auto same = [&](int r1, int r2) { return r1 / pl.R == r2 / pl.R; };
+        const bool rob = (kind == KFP_ROBIN);
+        bool bad = false;
+        if (sd.iL_tr != -2) bad |= rob ? (sd.iL_tr < 0 || sd.iL_tr + 1 >= sd.n || !same(sd.iL_tr, sd.iL_tr + 1))
+                                       : (sd.iL_tr < -1 || sd.iL_tr >= sd.n);
+        if (sd.iR_tr != -2) bad |= rob ? (sd.iR_tr - 1 < 0 || sd.iR_tr >= sd.n || !same(sd.iR_tr, sd.iR_tr - 1))
+                                       : (sd.iR_tr < 0 || sd.iR_tr > sd.n);
+        if (bad) {
+            set_err("kfp_swr_setup: trace stencil of subdomain %d straddles a row block (overlap too large for R=%d)",
+                    s_begin + i, pl.R);
+            return KFP_E_INVAL;
+        }
+    }
+    if (kfp_status st = ensure_qtab(pb, pl.R + 2)) return st;
+    if (kfp_status st = configure_kernels(pl)) return st;
+
+    // slabs and traces
+    std::vector<double *> toL(2 * std::max(0, nloc - 1)), toR(2 * std::max(0, nloc - 1));
+    for (int i = 0; i < nloc; ++i) {
+        SubDev &sd = pb->subs[i];
+        const size_t rows = (size_t)(sd.hi - sd.lo + 1);
+        for (int q = 0; q < 2; ++q)
+            if (kfp_status st = swr_alloc(pb, &sd.slab[q], rows * nx)) return st;
+    }
+    for (int i = 0; i + 1 < nloc; ++i)
+        for (int q = 0; q < 2; ++q) {
+            if (kfp_status st = swr_alloc(pb, &toL[2 * i + q], TR)) return st;
+            if (kfp_status st = swr_alloc(pb, &toR[2 * i + q], TR)) return st;
+            if (q == 0) {
+                pb->zero_on_reset.push_back(toL[2 * i]);
+                pb->zero_on_reset.push_back(toR[2 * i]);
+            }
+        }
+    for (int i = 0; i < nloc; ++i) {
+        SubDev &sd = pb->subs[i];
+        for (int q = 0; q < 2; ++q) {
+            if (i + 1 < nloc) {
+                sd.gR[q] = toL[2 * i + q];
+                sd.sendR[q] = toR[2 * i + q];
+            }
+            if (i > 0) {
+                sd.gL[q] = toR[2 * (i - 1) + q];
+                sd.sendL[q] = toL[2 * (i - 1) + q];
+            }
+        }
+    }
+    // cross-block edges
+    if (s_begin > 0)
+        for (int q = 0; q < 2; ++q) {
+            if (kfp_status st = swr_alloc(pb, &pb->edge_sendL[q], TR)) return st;
+            if (kfp_status st = swr_alloc(pb, &pb->edge_recvL[q], TR)) return st;
+            pb->subs[0].gL[q] = pb->edge_recvL[q];
+            pb->subs[0].sendL[q] = pb->edge_sendL[q];
+        }
+    if (s_end < n_sub)
+        for (int q = 0; q < 2; ++q) {
+            if (kfp_status st = swr_alloc(pb, &pb->edge_sendR[q], TR)) return st;
+            if (kfp_status st = swr_alloc(pb, &pb->edge_recvR[q], TR)) return st;
+            pb->subs[nloc - 1].gR[q] = pb->edge_recvR[q];
+            pb->subs[nloc - 1].sendR[q] = pb->edge_sendR[q];
+        }
+    {
+        void *q = nullptr;
+        KFP_CUDA(cudaMalloc(&q, sizeof(SubDev) * nloc));
+        pb->d_subs = static_cast<SubDev *>(q);
+        KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max));
+        pb->d_errT = static_cast<unsigned long long *>(q);
+        KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max));
+        pb->d_errIF = static_cast<unsigned long long *>(q);
+    }
+    KFP_CUDA(cudaMemcpy(pb->d_subs, pb->subs.data(), sizeof(SubDev) * nloc, cudaMemcpyHostToDevice));
+    if (kfp_status st = alloc_general_scratch(pb, pl, nloc, &pb->d_blkagg, &pb->d_chkagg, &pb->d_carry, pb->swr_allocs))
+        return st;
+    pb->setup = true;
+    if (kfp_status st = kfp_swr_reset(pb)) return st;
+    g_err = warn;
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_reset(kfp_problem pb) {
+    if (!pb || !pb->setup) {
+        set_err("kfp_swr_reset: no setup");
+        return KFP_E_STATE;
+    }
+    KFP_CUDA(cudaSetDevice(pb->device));
+    const size_t TR = (size_t)pb->nt * pb->nx;
+    for (double *p : pb->zero_on_reset) KFP_CUDA(cudaMemsetAsync(p, 0, TR * sizeof(double), pb->stream));
+    if (pb->edge_recvL[0]) KFP_CUDA(cudaMemsetAsync(pb->edge_recvL[0], 0, TR * sizeof(double), pb->stream));
+    if (pb->edge_recvR[0]) KFP_CUDA(cudaMemsetAsync(pb->edge_recvR[0], 0, TR * sizeof(double), pb->stream));
+    KFP_CUDA(cudaMemsetAsync(pb->d_errT, 0, sizeof(unsigned long long) * pb->K_max, pb->stream));
+    KFP_CUDA(cudaMemsetAsync(pb->d_errIF, 0, sizeof(unsigned long long) * pb->K_max, pb->stream));
+    pb->k_done = 0;
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
+    if (!pb || !pb->setup) {
+        set_err("kfp_swr_iterate: no setup");
+        return KFP_E_STATE;
+    }
+    if (n_iter < 0 || pb->k_done + n_iter > pb->K_max) {
+        set_err("kfp_swr_iterate: %d + %d iterations exceed K_max=%d", pb->k_done, n_iter, pb->K_max);
+        return KFP_E_STATE;
+    }
+    KFP_CUDA(cudaSetDevice(pb->device));
+    const int need = 2 + 2 * n_iter;
+    while ((int)pb->ev.size() < need) {
+        cudaEvent_t e;
+        KFP_CUDA(cudaEventCreate(&e));
+        pb->ev.push_back(e);
+    }
+    pb->ev_used = need;
+    const int nloc = (int)pb->subs.size();
+    StepParams P = base_params(pb);
+    P.subs = pb->d_subs;
+    P.send_robin = (pb->kind == KFP_ROBIN);
+    P.p = pb->p;
+    P.UT = pb->d_UT;
+    P.Ulines = pb->d_Ulines;
+    P.blkagg = pb->d_blkagg;
+    P.chkagg = pb->d_chkagg;
+    P.carry = pb->d_carry;
+    KFP_CUDA(cudaEventRecord(pb->ev[0], pb->stream));
+    for (int it = 0; it < n_iter; ++it) {
+        const int k = pb->k_done + 1;  // 1-based iteration number
+        P.par_in = (k - 1) & 1;
+        P.par_out = k & 1;
+        P.errT = pb->d_errT + (k - 1);
+        P.errIF = pb->d_errIF + (k - 1);
+        KFP_CUDA(cudaEventRecord(pb->ev[2 + 2 * it], pb->stream));
+        for (int n = 0; n < pb->nt; ++n) {
+            P.last = (n + 1 == pb->nt);
+            if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n)) return st;
+        }
+        KFP_CUDA(cudaEventRecord(pb->ev[3 + 2 * it], pb->stream));
+        pb->k_done = k;
+    }
+    KFP_CUDA(cudaEventRecord(pb->ev[1], pb->stream));
+    return KFP_OK;
+}
+
+kfp_status kfp_last_timing(kfp_problem pb, double *iterate_ms, double *kernel_ms) {
+    if (!pb || pb->ev_used < 2) {
+        set_err("kfp_last_timing: nothing timed yet");
+        return KFP_E_STATE;
+    }
+    KFP_CUDA(cudaEventSynchronize(pb->ev[1]));
+    float ms = 0;
+    KFP_CUDA(cudaEventElapsedTime(&ms, pb->ev[0], pb->ev[1]));
+    if (iterate_ms) *iterate_ms = ms;
+    if (kernel_ms) {
+        double tot = 0;
+        for (int i = 2; i + 1 < pb->ev_used; i += 2) {
+            KFP_CUDA(cudaEventElapsedTime(&ms, pb->ev[i], pb->ev[i + 1]));
+            tot += ms;
+        }
+        *kernel_ms = tot;
+    }
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_edge_buffers(kfp_problem pb, int32_t parity, double **send_left, double **recv_left,
+                                double **send_right, double **recv_right) {
+    if (!pb || !pb->setup || parity < 0 || parity > 1) {
+        set_err("kfp_swr_edge_buffers: no setup or bad parity");
+        return KFP_E_STATE;
+    }
+    if (send_left) *send_left = pb->edge_sendL[parity];
+    if (recv_left) *recv_left = pb->edge_recvL[parity];
+    if (send_right) *send_right = pb->edge_sendR[parity];
+    if (recv_right) *recv_right = pb->edge_recvR[parity];
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_bind_edge_buffers(kfp_problem pb, int32_t parity, double *send_left, double *recv_left,
+                                     double *send_right, double *recv_right) {
+    if (!pb || !pb->setup || parity < 0 || parity > 1) {
+        set_err("kfp_swr_bind_edge_buffers: no setup or bad parity");
+        return KFP_E_STATE;
+    }
+    const bool hasL = pb->s_begin > 0, hasR = pb->s_end < pb->S;
+    if ((!hasL && (send_left || recv_left)) || (!hasR && (send_right || recv_right))) {
+        set_err("kfp_swr_bind_edge_buffers: buffer given for a side without a neighbour block");
+        return KFP_E_INVAL;
+    }
+    const int nloc = (int)pb->subs.size();
+    if (send_left) pb->edge_sendL[parity] = pb->subs[0].sendL[parity] = send_left;
+    if (recv_left) pb->edge_recvL[parity] = recv_left, pb->subs[0].gL[parity] = recv_left;
+    if (send_right) pb->edge_sendR[parity] = pb->subs[nloc - 1].sendR[parity] = send_right;
+    if (recv_right) pb->edge_recvR[parity] = recv_right, pb->subs[nloc - 1].gR[parity] = recv_right;
+    KFP_CUDA(cudaMemcpyAsync(pb->d_subs, pb->subs.data(), sizeof(SubDev) * nloc, cudaMemcpyHostToDevice, pb->stream));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    if (parity == 0) return kfp_swr_reset(pb);
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_solve(kfp_problem pb, kfp_kind kind, double p, int32_t overlap, int32_t n_sub, int32_t K,
+                         double *uT) {
+    if (kfp_status st = kfp_swr_setup(pb, kind, p, overlap, n_sub, 0, n_sub, K)) return st;
+    std::string warn = g_err;
+    if (kfp_status st = kfp_swr_iterate(pb, K)) return st;
+    if (uT) {
+        const size_t nx = pb->nx;
+        const int par = pb->nt & 1;
+        for (int s = 0; s < n_sub; ++s) {
+            const SubDev &sd = pb->subs[s];
+            const int c0 = s * (pb->nv / n_sub);
+            const int c1 = (s == n_sub - 1) ? pb->nv : (s + 1) * (pb->nv / n_sub) - 1;
+            KFP_CUDA(cudaMemcpyAsync(uT + (size_t)c0 * nx, sd.slab[par] + (size_t)(c0 - sd.lo) * nx,
+                                     sizeof(double) * (size_t)(c1 - c0 + 1) * nx, cudaMemcpyDeviceToHost, pb->stream));
+        }
+    }
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    g_err = warn;
+    return KFP_OK;
+}
+
+kfp_status kfp_error_history(kfp_problem pb, int32_t cap, int32_t *K_out, double *err_T, double *err_if) {
+    if (!pb || !pb->setup || pb->k_done == 0) {
+        set_err("kfp_error_history: no iteration has run");
+        return KFP_E_STATE;
+    }
+    std::vector<unsigned long long> a(pb->k_done), b(pb->k_done);
+    KFP_CUDA(cudaMemcpyAsync(a.data(), pb->d_errT, sizeof(unsigned long long) * pb->k_done, cudaMemcpyDeviceToHost, pb->stream));
+    KFP_CUDA(cudaMemcpyAsync(b.data(), pb->d_errIF, sizeof(unsigned long long) * pb->k_done, cudaMemcpyDeviceToHost, pb->stream));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    if (K_out) *K_out = pb->k_done;
+    for (int k = 0; k < std::min<int>(cap, pb->k_done); ++k) {
+        double x, y;
+        std::memcpy(&x, &a[k], 8);
+        std::memcpy(&y, &b[k], 8);
+        if (err_T) err_T[k] = x;
+        if (err_if) err_if[k] = y;
+    }
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_subdomain_range(kfp_problem pb, int32_t s, int32_t *lo, int32_t *hi) {
+    if (!pb || !pb->setup || s < 0 || s >= pb->S) {
+        set_err("kfp_swr_subdomain_range: bad subdomain");
+        return KFP_E_INVAL;
+    }
+    if (lo) *lo = pb->lo[s];
+    if (hi) *hi = pb->hi[s];
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_subdomain_uT(kfp_problem pb, int32_t s, double *out) {
+    if (!pb || !pb->setup || s < pb->s_begin || s >= pb->s_end || !out) {
+        set_err("kfp_swr_subdomain_uT: subdomain %d not local", s);
+        return KFP_E_INVAL;
+    }
+    const SubDev &sd = pb->subs[s - pb->s_begin];
+    KFP_CUDA(cudaMemcpyAsync(out, sd.slab[pb->nt & 1], sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
+                             cudaMemcpyDeviceToHost, pb->stream));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_trace(kfp_problem pb, int32_t i, int32_t dir, double *out) {
+    if (!pb || !pb->setup || i < pb->s_begin || i + 1 >= pb->s_end || dir < 0 || dir > 1 || !out || pb->k_done == 0) {
+        set_err("kfp_swr_trace: interface %d not local or no iteration", i);
+        return KFP_E_INVAL;
+    }
+    const int par = pb->k_done & 1;
+    const SubDev &sd = pb->subs[i - pb->s_begin];
+    const double *src = (dir == 0) ? sd.gR[par] : sd.sendR[par];
+    KFP_CUDA(cudaMemcpyAsync(out, src, sizeof(double) * (size_t)pb->nt * pb->nx, cudaMemcpyDeviceToHost, pb->stream));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    return KFP_OK;
+}
+
+int64_t kfp_launch_count(kfp_problem pb) { return pb ? pb->launches : -1; }
+
+const char *kfp_plan(kfp_problem pb) {
+    if (!pb) return "";
+    pb->plan_text = pb->plan.text;
+    return pb->plan_text.c_str();
+}
+
+}  // extern "C"

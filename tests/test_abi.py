@@ -1,0 +1,78 @@
+"""-m "not gpu": the C-ABI library builds, loads and exports every symbol include/kfp.h declares;
+argument validation paths that need no device."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1306_4596_b200 import build, kfp
+
+    build.build()
+    return kfp.load()
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "kfp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return set(re.findall(r"\b(kfp_[A-Za-z_0-9]+)\s*\(", src))
+
+
+def test_header_symbols_exported(lib):
+    from paper_1306_4596_b200 import kfp
+
+    declared = _declared()
+    assert declared == set(kfp.SYMBOLS), declared ^ set(kfp.SYMBOLS)
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_sm100a_code_only():
+    from paper_1306_4596_b200 import build
+
+    assert "arch=compute_100a,code=sm_100a" in " ".join(build.FLAGS)
+
+
+def test_create_validation_without_device(lib):
+    """Invalid descriptions are rejected before any device work; a valid one fails loudly without a GPU."""
+    import kfp_inputs as ki
+    from paper_1306_4596_b200 import kfp
+
+    prob = ki.make_problem(ki.config("c0"))
+    with pytest.raises(kfp.KfpError) as e:
+        kfp.Problem(ki.make_problem(ki.scaled(ki.config("c0"), nx=63)))
+    assert e.value.status == kfp.KFP_E_INVAL
+    with pytest.raises(kfp.KfpError) as e:  # CFL: Vmax dt / h_x = 4 * 0.25/10 * 64 > 1
+        kfp.Problem(ki.make_problem(ki.scaled(ki.config("c0"), nt=10)))
+    assert e.value.status == kfp.KFP_E_CFL
+    try:
+        import torch
+
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if not has_gpu:
+        with pytest.raises(kfp.KfpError) as e:
+            kfp.Problem(prob)
+        assert e.value.status == kfp.KFP_E_CUDA
+
+
+def test_product_path_does_not_import_oracle():
+    """The product package never imports the oracle (and vice versa)."""
+    pkg = os.path.join(ROOT, "paper_1306_4596_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "liborc" not in txt, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".c")):
+            txt = open(os.path.join(ROOT, "oracle", f)).read()
+            assert "import paper_1306_4596_b200" not in txt and "from paper_1306_4596_b200" not in txt, f
+            assert "libkfp" not in txt, f

@@ -1,0 +1,188 @@
+"""-m gpu: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): max-abs relative error <= 1e-9 in fp64 for the
+solution and for the per-iteration error histories.  "Max-abs relative" is
+||a - b||_inf / ||b||_inf per array (reading R14): per u(T) slab and
+per history vector (normalised by its max).  Late history entries sit at the
+round-off floor (~1e-13 of err[1]) where two correct implementations differ in
+their digits, which is why the vector norm is used (SURVEY.md §7 hard part 4).
+"""
+from __future__ import annotations
+
+import functools
+
+import numpy as np
+import pytest
+
+import kfp_inputs as ki
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def kfp():
+    from paper_1306_4596_b200 import build, kfp as k
+
+    build.build()
+    k.load()
+    return k
+
+
+@functools.lru_cache(maxsize=None)
+def _oracle(run):
+    import oracle
+
+    return oracle.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, run.K, want_traces=True)
+
+
+def _gpu(kfp, run):
+    prob = ki.make_problem(run)
+    with kfp.Problem(prob) as pb:
+        uT = pb.solve(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        eT, eI = pb.history()
+        slabs = [pb.subdomain_uT(s) for s in range(run.n_sub)]
+        UT = pb.monodomain_uT()
+        traces = []
+        for i in range(run.n_sub - 1):
+            traces += [pb.trace(i, 0), pb.trace(i, 1)]
+        plan = pb.plan()
+    return dict(uT=uT, err_T=eT, err_if=eI, uT_sub=slabs, UT=UT, traces=traces, plan=plan)
+
+
+def _compare(g, r, name):
+    assert rel(g["UT"], r["UT"]) <= TOL, name
+    assert rel(g["uT"], r["uT"]) <= TOL, name
+    for s, (a, b) in enumerate(zip(g["uT_sub"], r["uT_sub"])):
+        assert rel(a, b) <= TOL, (name, s)
+    assert rel(g["err_T"], r["err_T"]) <= TOL, (name, g["err_T"], r["err_T"])
+    assert rel(g["err_if"], r["err_if"]) <= TOL, (name, g["err_if"], r["err_if"])
+    if r["traces"] is not None:
+        for i, t in enumerate(g["traces"]):
+            assert rel(t, r["traces"][i]) <= TOL, (name, "trace", i)
+
+
+CASES = {
+    # BASELINE.json configs[0] and [1] at full size
+    "c0": ki.config("c0"),
+    "c1": ki.config("c1"),
+    # ragged tail in x (70 = 2*32 + 6 columns) and tiny subdomains
+    "ragged_robin": ki.scaled(ki.config("c0"), nx=70, nv=48, nt=120, K=6, name="ragged_robin").with_(n_sub=3),
+    "ragged_dirichlet_ov": ki.scaled(ki.config("c1"), nx=38, nv=96, nt=200, K=8, name="ragged_dir").with_(
+        n_sub=4, overlap=6),
+    # Dirichlet without overlap (the non-converging classical case)
+    "dirichlet_ov0": ki.config("c0").with_(name="dir_ov0", kind="dirichlet", p=0.0, K=5),
+    # Robin with overlap (OSWR with L = 3 h_v)
+    "robin_ov3": ki.scaled(ki.config("c1"), nt=300, K=6, name="robin_ov3").with_(kind="robin", p=4.23, overlap=3),
+    # BASELINE configs[4] structure (S=32, 4-cell overlap, random f >= 0, u0 = 0) at oracle size
+    "c4_small": ki.scaled(ki.config("c4"), nx=64, nv=32 * 32, nt=60, K=6, name="c4_small"),
+    # one subdomain (must equal the monodomain), several row blocks per column
+    "single_sub": ki.scaled(ki.config("c0"), nv=1200, nt=100, name="single").with_(n_sub=1, K=1),
+    # columns taller than one cluster -> three-phase path
+    "three_phase": ki.scaled(ki.config("c2"), nx=64, nv=4400, nt=40, K=3, name="three_phase").with_(n_sub=1),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_parity_vs_oracle(kfp, name):
+    run = CASES[name]
+    g = _gpu(kfp, run)
+    r = _oracle(run)
+    _compare(g, r, name)
+
+
+def test_single_subdomain_equals_monodomain(kfp):
+    run = CASES["single_sub"]
+    g = _gpu(kfp, run)
+    assert np.array_equal(g["uT"], g["UT"])  # same kernels, same arithmetic: bitwise
+
+
+def test_deterministic(kfp):
+    run = CASES["c4_small"]
+    a, b = _gpu(kfp, run), _gpu(kfp, run)
+    assert np.array_equal(a["uT"], b["uT"]) and np.array_equal(a["err_T"], b["err_T"])
+    assert np.array_equal(a["err_if"], b["err_if"])
+
+
+def test_block_split_matches_single_process(kfp):
+    """The edge-buffer protocol of the multi-GPU path (kfp_swr_edge_buffers), emulated with two
+    problems on one device and device-to-device copies standing in for NCCL send/recv: results
+    must be bitwise identical to one process owning every subdomain."""
+    import torch
+
+    run = ki.scaled(ki.config("c4"), nx=64, nv=16 * 64, nt=50, K=4, name="split").with_(n_sub=16)
+    prob = ki.make_problem(run)
+    full = _gpu(kfp, run)
+    A = kfp.Problem(prob)
+    B = kfp.Problem(prob)
+    A.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, 0, 8)
+    B.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, 8, 16)
+    shape = (run.grid.nt, run.grid.nx)
+    bufs = {key: [torch.zeros(shape, dtype=torch.float64, device="cuda") for _ in range(2)]
+            for key in ("a_send", "a_recv", "b_send", "b_recv")}
+    for par in (0, 1):
+        A.bind_edge_buffers(par, send_right=bufs["a_send"][par].data_ptr(), recv_right=bufs["a_recv"][par].data_ptr())
+        B.bind_edge_buffers(par, send_left=bufs["b_send"][par].data_ptr(), recv_left=bufs["b_recv"][par].data_ptr())
+    for k in range(1, run.K + 1):
+        A.iterate(1)
+        B.iterate(1)
+        torch.cuda.synchronize()
+        bufs["b_recv"][k & 1].copy_(bufs["a_send"][k & 1])  # stands in for NCCL send/recv
+        bufs["a_recv"][k & 1].copy_(bufs["b_send"][k & 1])
+        torch.cuda.synchronize()
+    eTa, eIa = A.history()
+    eTb, eIb = B.history()
+    assert np.array_equal(np.maximum(eTa, eTb), full["err_T"])
+    assert np.array_equal(np.maximum(eIa, eIb), full["err_if"])
+    for s in range(16):
+        sl = (A if s < 8 else B).subdomain_uT(s)
+        assert np.array_equal(sl, full["uT_sub"][s]), s
+    A.close()
+    B.close()
+
+
+def test_c2_full_size_vs_mode_reduced_oracle(kfp):
+    """BASELINE.json configs[2] at full size (the bench workload, same launch plan), against the
+    mode-reduced oracle (exact for the manufactured data, oracle/modal.py): every output element."""
+    from oracle.modal import max_abs_real, modal_swr, realize
+
+    run = ki.config("c2")
+    g = _gpu(kfp, run)
+    m = modal_swr(run.grid, run.kind, run.p, run.overlap, run.n_sub, run.K)
+    for s in range(run.n_sub):
+        ref = realize(m["c_sub"][s], run.grid.nx)
+        assert rel(g["uT_sub"][s], ref) <= TOL, s
+    assert rel(g["UT"], realize(m["C"], run.grid.nx)) <= TOL
+    assert rel(g["err_T"], m["err_T"]) <= TOL
+    assert rel(g["err_if"], m["err_if"]) <= TOL
+
+
+def test_c4_full_size_properties(kfp):
+    """BASELINE.json configs[4] at full size on one GPU: discrete maximum principle and monotone
+    Schwarz iterates hold at any size: 0 <= u^k <= U, err
+    non-increasing in k, and the interface error bounds the error at T."""
+    run = ki.config("c4").with_(K=4)
+    prob = ki.make_problem(run)
+    with kfp.Problem(prob) as pb:
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        UT = pb.monodomain_uT()
+        prev = None
+        for k in range(run.K):
+            pb.iterate(1)
+            sl = [pb.subdomain_uT(s) for s in (0, 7, 16, 31)]
+            if prev is not None:
+                for a, b in zip(prev, sl):
+                    assert (a <= b + 1e-14).all()
+            prev = sl
+        eT, eI = pb.history()
+        for s, a in zip((0, 7, 16, 31), prev):
+            lo, hi = pb.subdomain_range(s)
+            assert a.min() >= 0.0
+            assert (a <= UT[lo:hi + 1] + 1e-14).all()
+    assert UT.min() >= 0.0
+    assert np.all(np.diff(eI) <= 0.0) and np.all(eT <= eI * (1 + 1e-12))
