@@ -15,8 +15,12 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "../../include/kfp.h"
 #include "kfp_device.cuh"
+#include "kfp_fused.cuh"
 
 using kfp::SubDev;
 using kfp::StepParams;
@@ -44,38 +48,99 @@ void set_err(const char *fmt, ...) {
     } while (0)
 
 struct Plan {
-    bool fused = false;
+    bool fused = false;  // fused TMA/cluster kernel; else the three-phase path
     int P = 8, b = 32, R = 256, C = 1;
+    int L = 0, B = 0, NR = 2;  // fused: chunk rows, register-array size (template), forcing ranks (template)
     size_t smem = 0;
     std::string text;
 };
 
-// Launch geometry for columns of at most n_max unknown rows:
-// P = 8 warps per CTA, chunks of b rows, row blocks of R = P b rows; C blocks
-// per column.  C <= 8 -> one thread-block cluster per 32-column tile (fused
-// kernel); otherwise the three-phase path with global block aggregates.
-Plan make_plan(int n_max, bool allow_fused) {
+using FusedKernel = void (*)(const kfp::FusedParams);
+constexpr int kBs[] = {8, 16, 17, 24, 32};
+
+template <int B, int NR>
+void fused_entry(FusedKernel *k, size_t *smem) {
+    *k = kfp::step_fused_tma<B, NR>;
+    *smem = kfp::fused_smem_bytes<B, NR>();
+}
+bool fused_kernel(int B, int NR, FusedKernel *k, size_t *smem) {
+#define KFP_ENTRY(BB)                                   \
+    if (B == BB && NR == 2) { fused_entry<BB, 2>(k, smem); return true; } \
+    if (B == BB && NR == 4) { fused_entry<BB, 4>(k, smem); return true; }
+    KFP_ENTRY(8) KFP_ENTRY(16) KFP_ENTRY(17) KFP_ENTRY(24) KFP_ENTRY(32)
+#undef KFP_ENTRY
+    return false;
+}
+
+// Launch geometry for columns of at most n_max unknown rows.
+// Fused path: P = 16 warps per CTA, chunks of L rows (target 17), row blocks of
+// R = 16 L rows, C = ceil(n_max / R) <= 8 CTAs per cluster.  Otherwise the
+// three-phase path (P = 8, b = 32, block aggregates through global memory).
+Plan make_plan(int n_max, int f_rank, bool allow_fused) {
     Plan pl;
-    pl.P = 8;
-    const int target = 256;
-    int C = (n_max + target - 1) / target;
-    if (allow_fused && C <= 8) {
+    const int P = kfp::kFusedWarps;
+    int C = (n_max + P * 17 - 1) / (P * 17);
+    if (C > 8) C = 8;
+    const int L = (n_max + P * C - 1) / (P * C);
+    int B = 0;
+    for (int bb : kBs)
+        if (bb >= L) {
+            B = bb;
+            break;
+        }
+    if (allow_fused && B > 0 && f_rank <= kfp::kNRmax) {
         pl.fused = true;
-        pl.C = std::max(1, C);
-        pl.b = (n_max + pl.C * pl.P - 1) / (pl.C * pl.P);
-        pl.b = std::max(pl.b, 2);
+        pl.P = P;
+        pl.C = C;
+        pl.L = L;
+        pl.B = B;
+        pl.NR = (f_rank <= 2) ? 2 : 4;
+        pl.b = L;
+        pl.R = P * L;
+        FusedKernel k;
+        fused_kernel(pl.B, pl.NR, &k, &pl.smem);
     } else {
         pl.fused = false;
+        pl.P = 8;
         pl.b = 32;
         pl.C = (n_max + pl.P * pl.b - 1) / (pl.P * pl.b);
+        pl.R = pl.P * pl.b;
+        pl.smem = kfp::smem_bytes(pl.R, pl.P);
     }
-    pl.R = pl.P * pl.b;
-    pl.smem = kfp::smem_bytes(pl.R, pl.P);
-    char buf[160];
-    snprintf(buf, sizeof buf, "%s P=%d b=%d R=%d C=%d smem=%zu", pl.fused ? "fused-cluster" : "three-phase", pl.P,
-             pl.b, pl.R, pl.C, pl.smem);
+    char buf[200];
+    if (pl.fused)
+        snprintf(buf, sizeof buf, "fused-tma-cluster P=%d L=%d (B=%d) R=%d C=%d NR=%d smem=%zu", pl.P, pl.L, pl.B, pl.R,
+                 pl.C, pl.NR, pl.smem);
+    else
+        snprintf(buf, sizeof buf, "three-phase P=%d b=%d R=%d C=%d smem=%zu", pl.P, pl.b, pl.R, pl.C, pl.smem);
     pl.text = buf;
     return pl;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// Tensor map of a slab's unknown rows: 2-D fp64 [n rows][nx], box (32 + 2*halo) x L.
+bool make_tmap(CUtensorMap *map, double *rows_base, int nx, int nrows, int L) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)nx, (cuuint64_t)nrows};
+    cuuint64_t strides[1] = {(cuuint64_t)nx * sizeof(double)};
+    cuuint32_t box[2] = {(cuuint32_t)kfp::kTW, (cuuint32_t)L};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, rows_base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
 }
 }  // namespace
 
@@ -111,6 +176,7 @@ struct kfp_problem_s {
     unsigned long long *d_errT = nullptr, *d_errIF = nullptr;
     Plan plan;
     double *d_blkagg = nullptr, *d_chkagg = nullptr, *d_carry = nullptr;
+    CUtensorMap *d_tmaps = nullptr;  // [nloc][2]
     std::vector<double *> swr_allocs;
     double *edge_sendL[2] = {nullptr, nullptr}, *edge_recvL[2] = {nullptr, nullptr};
     double *edge_sendR[2] = {nullptr, nullptr}, *edge_recvR[2] = {nullptr, nullptr};
@@ -144,6 +210,8 @@ void free_swr(kfp_problem pb) {
     if (pb->d_errIF) cudaFree(pb->d_errIF);
     pb->d_errT = pb->d_errIF = nullptr;
     pb->d_blkagg = pb->d_chkagg = pb->d_carry = nullptr;
+    if (pb->d_tmaps) cudaFree(pb->d_tmaps);
+    pb->d_tmaps = nullptr;
     for (int q = 0; q < 2; ++q) pb->edge_sendL[q] = pb->edge_recvL[q] = pb->edge_sendR[q] = pb->edge_recvR[q] = nullptr;
     pb->setup = false;
 }
@@ -263,8 +331,9 @@ StepParams base_params(kfp_problem pb) {
     return P;
 }
 
-// One time step of every subdomain in `subs` (device array of nsub entries).
-kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, int n) {
+// One time step of every subdomain in P.subs (nsub entries).
+kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, int n, const CUtensorMap *tmaps,
+                       int nrec = 0, const int *rec_rows = nullptr) {
     P.n = n;
     P.from_u0 = (n == 0);
     for (int r = 0; r < kfp::kMaxRank; ++r) P.cf[r] = (r < pb->f_rank) ? pb->dt * pb->ft[(size_t)r * (pb->nt + 1) + n + 1] : 0.0;
@@ -275,19 +344,30 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
     const int ntiles = (pb->nx + kfp::kWarp - 1) / kfp::kWarp;
     const dim3 block(pl.P * kfp::kWarp);
     if (pl.fused) {
+        kfp::FusedParams FP;
+        FP.S = P;
+        FP.tmaps = tmaps;
+        FP.L = pl.L;
+        FP.nrec = nrec;
+        FP.rec_rows = rec_rows;
+        FusedKernel k;
+        size_t smem;
+        fused_kernel(pl.B, pl.NR, &k, &smem);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(pl.C, ntiles, nsub);
         cfg.blockDim = block;
-        cfg.dynamicSmemBytes = pl.smem;
+        cfg.dynamicSmemBytes = smem;
         cfg.stream = pb->stream;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = pl.C;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        KFP_CUDA(cudaLaunchKernelEx(&cfg, kfp::step_fused, P));
+        cfg.numAttrs = 2;
+        KFP_CUDA(cudaLaunchKernelEx(&cfg, k, FP));
         pb->launches += 1;
     } else {
         kfp::step_phase1<<<dim3(pl.C, ntiles, nsub), block, pl.smem, pb->stream>>>(P);
@@ -299,10 +379,34 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
     return KFP_OK;
 }
 
+// Tensor maps of the slabs of nsub subdomains (host copy -> device array).
+kfp_status build_tmaps(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, CUtensorMap **out,
+                       std::vector<void *> *owner) {
+    *out = nullptr;
+    if (!pl.fused) return KFP_OK;
+    std::vector<CUtensorMap> maps(2 * subs.size());
+    for (size_t i = 0; i < subs.size(); ++i)
+        for (int q = 0; q < 2; ++q) {
+            double *base = subs[i].slab[q] + (size_t)(subs[i].first - subs[i].lo) * pb->nx;
+            if (!make_tmap(&maps[2 * i + q], base, pb->nx, subs[i].n, pl.L)) {
+                set_err("cuTensorMapEncodeTiled failed (nx=%d rows=%d L=%d)", pb->nx, subs[i].n, pl.L);
+                return KFP_E_CUDA;
+            }
+        }
+    void *d = nullptr;
+    KFP_CUDA(cudaMalloc(&d, sizeof(CUtensorMap) * maps.size()));
+    KFP_CUDA(cudaMemcpy(d, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
+    *out = static_cast<CUtensorMap *>(d);
+    if (owner) owner->push_back(d);
+    return KFP_OK;
+}
+
 kfp_status configure_kernels(const Plan &pl) {
     if (pl.fused) {
-        KFP_CUDA(cudaFuncSetAttribute(kfp::step_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-        if (pl.C > 8) KFP_CUDA(cudaFuncSetAttribute(kfp::step_fused, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        FusedKernel k;
+        size_t smem;
+        fused_kernel(pl.B, pl.NR, &k, &smem);
+        KFP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     } else {
         KFP_CUDA(cudaFuncSetAttribute(kfp::step_phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
         KFP_CUDA(cudaFuncSetAttribute(kfp::step_phase3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
@@ -363,9 +467,9 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     sd.slab[0] = pb->d_mono[0];
     sd.slab[1] = pb->d_mono[1];
     woodbury(pb, sd, 0.0);
-    Plan pl = make_plan(sd.n, true);
+    Plan pl = make_plan(sd.n, pb->f_rank, true);
     sd.nblk = (sd.n + pl.R - 1) / pl.R;
-    if (kfp_status st = ensure_qtab(pb, pl.R + 2)) return st;
+    if (kfp_status st = ensure_qtab(pb, std::max(pl.R, sd.n) + 2)) return st;
     if (kfp_status st = configure_kernels(pl)) return st;
     SubDev *d_sd = nullptr;
     std::vector<double *> tmp;
@@ -377,11 +481,25 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     P.line_of_node = pb->d_line_of_node;
     P.rec = pb->d_Ulines;
     P.last = 0;  // no error accumulation on the reference itself; end rows stay 0 (memset)
+    std::vector<void *> tmp2;
+    CUtensorMap *d_maps = nullptr;
+    int *d_rec = nullptr;
+    std::vector<int> rec_rows(lines.size());
+    for (size_t i = 0; i < lines.size(); ++i) rec_rows[i] = lines[i] - sd.first;
     kfp_status st = alloc_general_scratch(pb, pl, 1, &P.blkagg, &P.chkagg, &P.carry, tmp);
-    for (int n = 0; st == KFP_OK && n < pb->nt; ++n) st = launch_step(pb, pl, P, 1, n);
+    if (!st) st = build_tmaps(pb, pl, std::vector<SubDev>{sd}, &d_maps, &tmp2);
+    if (!st && !rec_rows.empty()) {
+        if (cudaMalloc(&d_rec, sizeof(int) * rec_rows.size()) != cudaSuccess ||
+            cudaMemcpy(d_rec, rec_rows.data(), sizeof(int) * rec_rows.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+            st = KFP_E_CUDA;
+    }
+    for (int n = 0; st == KFP_OK && n < pb->nt; ++n)
+        st = launch_step(pb, pl, P, 1, n, d_maps, (int)rec_rows.size(), d_rec);
     cudaError_t e = cudaStreamSynchronize(pb->stream);
     cudaFree(d_sd);
+    if (d_rec) cudaFree(d_rec);
     for (double *q : tmp) cudaFree(q);
+    for (void *q : tmp2) cudaFree(q);
     if (st != KFP_OK) return st;
     KFP_CUDA(e);
     pb->d_UT = pb->d_mono[pb->nt & 1];
@@ -632,7 +750,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
         woodbury(pb, sd, p);
         n_max = std::max(n_max, sd.n);
     }
-    pb->plan = make_plan(n_max, true);
+    pb->plan = make_plan(n_max, pb->f_rank, true);
     const Plan &pl = pb->plan;
     // the rows of each outgoing trace stencil must sit in one row block
     for (int i = 0; i < nloc; ++i) {
@@ -651,7 +769,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
             return KFP_E_INVAL;
         }
     }
-    if (kfp_status st = ensure_qtab(pb, pl.R + 2)) return st;
+    if (kfp_status st = ensure_qtab(pb, std::max(pl.R, n_max) + 2)) return st;
     if (kfp_status st = configure_kernels(pl)) return st;
 
     // slabs and traces
@@ -709,6 +827,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
         pb->d_errIF = static_cast<unsigned long long *>(q);
     }
     KFP_CUDA(cudaMemcpy(pb->d_subs, pb->subs.data(), sizeof(SubDev) * nloc, cudaMemcpyHostToDevice));
+    if (kfp_status st = build_tmaps(pb, pl, pb->subs, &pb->d_tmaps, nullptr)) return st;
     if (kfp_status st = alloc_general_scratch(pb, pl, nloc, &pb->d_blkagg, &pb->d_chkagg, &pb->d_carry, pb->swr_allocs))
         return st;
     pb->setup = true;
@@ -770,7 +889,7 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
         KFP_CUDA(cudaEventRecord(pb->ev[2 + 2 * it], pb->stream));
         for (int n = 0; n < pb->nt; ++n) {
             P.last = (n + 1 == pb->nt);
-            if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n)) return st;
+            if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n, pb->d_tmaps)) return st;
         }
         KFP_CUDA(cudaEventRecord(pb->ev[3 + 2 * it], pb->stream));
         pb->k_done = k;

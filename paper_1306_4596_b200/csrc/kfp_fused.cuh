@@ -1,0 +1,521 @@
+// kfp_fused.cuh -- the hot kernel: one fused time step of every local subdomain
+// (transport + forcing + v-tridiagonal solve + transmission traces + errors),
+// sm_100a, TMA tile loads, register-resident chunks, cluster (DSMEM) carries.
+//
+// Geometry.  A cluster of C CTAs owns one 32-column x-tile of one
+// subdomain's column stack; CTA `blk` owns the unknown rows [blk*R, blk*R+R),
+// R = P*L; warp w owns the chunk of L <= B rows starting at blk*R + w*L, lane =
+// x-column.  The chunk lives in registers through the three passes:
+//   A  r' = (q/a)[(1-|nu|) u + |nu| u_nb + dt f]  and the forward scan
+//      h_l = q h_{l-1} + r'_l (zero carry)                       (P:496-516 + B^{-1} part 1)
+//   B  backward scan k_l = q k_{l+1} + h_l (zero carry)          (B^{-1} part 2)
+//   C  x_l = k_l + kap(l, L) Y + q^{L-l} X with the chunk carries Y (y just above
+//      the chunk) and X (x just below it).
+// The carries of a linear constant-coefficient recurrence are closed-form sums
+// of powers of q over the preceding / following chunks, so every warp computes
+// its own from the other chunks' end values (no serial chain); the same holds
+// across the CTAs of the cluster (distributed shared memory) and for the two
+// Woodbury boundary terms of the column system (kfp_device.cuh header).
+// u^n arrives by one cp.async.bulk.tensor (TMA) per warp: a box of (2+32+2) x L
+// fp64 (the tile plus a 2-column halo on each side) into shared memory; the
+// upwind neighbour is then a shared-memory load at lane +- 1.
+#pragma once
+#include <cuda.h>
+
+#include "kfp_device.cuh"
+
+namespace kfp {
+
+// halo columns per side in the smem tile: 2, so that the TMA box starts on a
+// 16-B aligned global column (a box starting at an odd column faults)
+constexpr int kHalo = 2;
+constexpr int kTW = kWarp + 2 * kHalo;       // 36 doubles (288 B) per smem tile row
+constexpr int kFusedWarps = 16;              // P
+constexpr int kNRmax = 4;                    // forcing ranks supported by the coefficient table
+constexpr int kMaxFusedCluster = 8;          // portable cluster size
+
+struct FusedParams {
+    StepParams S;                 // common step parameters (kfp_device.cuh)
+    const CUtensorMap *tmaps;     // [nsub][2] tensor maps of the slabs' unknown rows (by step parity)
+    int L;                        // chunk length (rows per warp), R = P*L rows per CTA
+    int nrec;                     // monodomain line recording: number of recorded rows
+    const int *rec_rows;          // [nrec] unknown-row index of each recorded line (in line order)
+};
+
+// --------------------------------------------------------------------------- PTX
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ double ld_dsmem(const double *local_addr, int rank) {
+    // read a double of CTA `rank`'s shared memory at the same offset as local_addr
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local_addr)), "r"(rank));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
+    return v;
+}
+
+// --------------------------------------------------------------------------- smem
+// per-warp tile slot: B rows of kTW doubles, padded to a multiple of 128 B (TMA destination alignment)
+template <int B>
+constexpr int slot_doubles() {
+    return ((B * kTW * 8 + 127) / 128) * 128 / 8;
+}
+constexpr int kQtab = kFusedWarps * 32 + 2;  // q^k and s2(k) for k <= R (R <= P * 32)
+
+template <int B, int NR>
+struct FusedSmem {
+    static constexpr int kSlot = slot_doubles<B>();
+    static constexpr int kRows = kFusedWarps * B;
+    static constexpr int kCoef = 2 + NR;   // c0', c1', g_0' .. g_{NR-1}'
+    alignas(128) double tile[kFusedWarps * kSlot];
+    double coef[kRows * kCoef];
+    double qp[kQtab], s2[kQtab];           // q^k, sum_{t<k} q^{2t}
+    double he[kFusedWarps * kWarp];        // y at the chunk's last row (zero carry)
+    double ks[kFusedWarps * kWarp];        // k at the chunk's first row (zero carry)
+    double Z0[kFusedWarps * kWarp];        // x at the chunk's first row, zero carries below / above the block
+    double kb[4 * kWarp];                  // k at the column's rows 0,1,n-2,n-1 (chunk-local zero carries)
+    double pub[6 * kWarp];                 // F, G, x~_0, x~_1, x~_{n-2}, x~_{n-1} (block-local) for the cluster
+    double cb[2 * kWarp];                  // this block's carries Y_blk, X_blk
+    double gin[2 * kWarp];                 // incoming traces at t_{n+1} (lo end, hi end)
+    double rtr[2 * kWarp];                 // raw r at the outgoing-trace rows
+    double red[2 * kFusedWarps];
+    uint64_t bar[kFusedWarps];
+};
+
+template <int B, int NR>
+__host__ __device__ constexpr size_t fused_smem_bytes() {
+    return sizeof(FusedSmem<B, NR>);
+}
+
+// --------------------------------------------------------------------------- passes
+// DIR = -1: every row of the chunk has v >= 0 (upwind neighbour m-1); +1: v < 0
+// (neighbour m+1); 0: generic (per-row side, ragged length).
+template <int B, int NR, int DIR>
+__device__ __forceinline__ void pass_a_reg(const double *tile_w, const double *coef_w, int lane, double q,
+                                           const double (&fx)[NR], double (&h)[B], int Lw, int jv2_0, double &hend) {
+    constexpr int kC = 2 + NR;
+    double hp = 0.0;
+#pragma unroll
+    for (int l = 0; l < B; ++l) {
+        const double *row = tile_w + l * kTW + kHalo + lane;
+        const double *c = coef_w + l * kC;
+        const double u = row[0];
+        double nb;
+        if (DIR == 0) {
+            const int off = (jv2_0 + 2 * l >= 0) ? -1 : 1;  // 2j - nv >= 0: v >= 0 -> left neighbour
+            nb = row[off];
+        } else {
+            nb = row[DIR];
+        }
+        double f = 0.0;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) f = fma(c[2 + r], fx[r], f);
+        const double rp = fma(c[1], nb, fma(c[0], u, f));
+        if (DIR == 0) {
+            h[l] = (l < Lw) ? fma(q, hp, rp) : 0.0;
+            hend = (l == Lw - 1) ? h[l] : hend;
+        } else {
+            h[l] = fma(q, hp, rp);
+        }
+        hp = h[l];
+    }
+    if (DIR != 0) hend = h[B - 1];
+}
+
+template <int B>
+__device__ __forceinline__ double pass_b_full(double (&h)[B], double q) {
+    double kn = 0.0;
+#pragma unroll
+    for (int l = B - 1; l >= 0; --l) {
+        kn = fma(q, kn, h[l]);
+        h[l] = kn;
+    }
+    return kn;
+}
+// Ragged chunk: rows l >= Lw are not part of the column; also captures k at
+// the chunk's last two rows.
+template <int B>
+__device__ __forceinline__ double pass_b_ragged(double (&h)[B], double q, int Lw, double &k_last, double &k_last2) {
+    double kn = 0.0;
+#pragma unroll
+    for (int l = B - 1; l >= 0; --l) {
+        kn = (l < Lw) ? fma(q, kn, h[l]) : 0.0;
+        h[l] = kn;
+        k_last = (l == Lw - 1) ? kn : k_last;
+        k_last2 = (l == Lw - 2) ? kn : k_last2;
+    }
+    return kn;
+}
+
+// response at row r (local) of the x-recurrence to a unit carry entering above row 0
+// of a segment of `len` rows: kap(r, len) = q^{r+1} s2(len - r)
+__device__ __forceinline__ double kap_s(const double *qp, const double *s2, int r, int len) {
+    return qp[r + 1] * s2[len - r];
+}
+
+// --------------------------------------------------------------------------- the kernel
+template <int B, int NR>
+__global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const FusedParams FP) {
+    using Sm = FusedSmem<B, NR>;
+    extern __shared__ __align__(128) char smraw[];
+    Sm &sm = *reinterpret_cast<Sm *>(smraw);
+    const StepParams &P = FP.S;
+    const int blk = static_cast<int>(cg::this_cluster().block_rank());
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = blockIdx.z;
+    const SubDev &S = P.subs[sub];
+    const int n = S.n, L = FP.L, R = kFusedWarps * L;
+    const int m0 = blockIdx.y * kWarp, w = min(kWarp, P.nx - m0);
+    const int m = m0 + min(lane, w - 1);
+    const bool active = lane < w;
+    const int rb0 = blk * R;                                    // first unknown row of this block
+    const int Rb = max(0, min(R, n - rb0));                     // rows of this block
+    const int s_w = warp * L;                                   // chunk start (block-local)
+    const int Lw = max(0, min(L, Rb - s_w));                    // rows of this warp's chunk
+    const int e_w = s_w + Lw;                                   // chunk end (block-local, exclusive)
+    const int cr0 = rb0 + s_w;                                  // first column row of the chunk
+    const int nblk = S.nblk;
+    const double q = P.q;
+    const CUtensorMap *tmap = FP.tmaps + 2 * sub + (P.n & 1);
+    double *unew_slab = S.slab[(P.n + 1) & 1];
+    double *unew = unew_slab + static_cast<size_t>(S.first - S.lo) * P.nx;
+    double *tile_w = sm.tile + warp * Sm::kSlot;
+    const size_t goff = static_cast<size_t>(P.n) * P.nx + m;   // row t_{n+1} of [nt][nx] arrays
+
+    // ---- prologue: constant tables only (overlaps the previous step under PDL)
+    if (lane == 0) {
+        mbar_init(&sm.bar[warp], 1);
+        if (warp == 0) prefetch_tmap(tmap);
+    }
+    fence_mbar_init();
+    for (int rr = threadIdx.x; rr < Rb; rr += blockDim.x) {    // per-row coefficients, scaled by q/a
+        const int slot = (rr / L) * B + (rr % L);
+        const int j = S.first + rb0 + rr;
+        const double2 rc = __ldg(P.rowc + j);
+        double *c = sm.coef + slot * Sm::kCoef;
+        c[0] = P.qa * rc.x;
+        c[1] = P.qa * rc.y;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) c[2 + r] = (r < P.f_rank) ? P.qa * P.cf[r] * __ldg(P.fv + r * (P.nv + 1) + j) : 0.0;
+    }
+    for (int k = threadIdx.x; k <= R + 1 && k < kQtab; k += blockDim.x) {
+        sm.qp[k] = __ldg(P.qp + k);
+        sm.s2[k] = __ldg(P.s2 + k);
+    }
+    double fx[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) fx[r] = (r < P.f_rank) ? __ldg(P.fx + r * P.nx + m) : 0.0;
+    // incoming traces of this step (written by the previous iteration, complete before this launch chain)
+    if (warp == 0) {
+        sm.gin[lane] = (S.ltype != END_PHYS) ? S.gL[P.par_in][goff] : 0.0;
+        sm.gin[kWarp + lane] = (S.rtype != END_PHYS) ? S.gR[P.par_in][goff] : 0.0;
+    }
+
+    // ---- wait for the previous step, then load this warp's chunk with one TMA
+    grid_dep_wait();
+    __syncthreads();
+    if (Lw > 0 && !P.from_u0 && lane == 0) {
+        mbar_expect_tx(&sm.bar[warp], static_cast<uint32_t>(kTW * L * sizeof(double)));
+        tma_load_2d(tile_w, tmap, m0 - kHalo, cr0, &sm.bar[warp]);
+    }
+
+    double h[B];
+    double hend = 0.0, kst = 0.0, eif = 0.0, et = 0.0;
+    if (Lw > 0) {
+        if (P.from_u0) {  // u^0 from the separable u0 tables (0 B of HBM), incl. the halo columns
+            for (int l = 0; l < Lw; ++l) {
+                const int j = S.first + cr0 + l;
+                for (int c = lane; c < kTW; c += kWarp) {
+                    const int mm = ((m0 - kHalo + c) % P.nx + P.nx) % P.nx;
+                    double s = 0.0;
+                    for (int r = 0; r < P.u0_rank; ++r)
+                        s = fma(__ldg(P.u0v + r * (P.nv + 1) + j), __ldg(P.u0x + r * P.nx + mm), s);
+                    tile_w[l * kTW + c] = s;
+                }
+            }
+            __syncwarp();
+        } else {
+            mbar_wait(&sm.bar[warp], 0);
+            // periodic wrap of the halo at the ends of the x range (TMA zero-fills out-of-range columns)
+            const double *src = S.slab[P.n & 1] + static_cast<size_t>(S.first - S.lo + cr0) * P.nx;
+            if (m0 == 0 && lane < Lw) tile_w[lane * kTW + kHalo - 1] = src[static_cast<size_t>(lane) * P.nx + P.nx - 1];
+            if (m0 + w == P.nx && lane < Lw) tile_w[lane * kTW + kHalo + w] = src[static_cast<size_t>(lane) * P.nx];
+            __syncwarp();
+        }
+        const int jv2_0 = 2 * (S.first + cr0) - P.nv;          // 2 j - nv of the chunk's first row
+        const int jv2_1 = jv2_0 + 2 * (Lw - 1);
+        // full chunks take the unpredicated paths; the chunk holding the column's
+        // last two rows takes the ragged one (it captures their k values)
+        const bool full = (Lw == B) && (cr0 + Lw <= n - 2);
+        const double *coef_w = sm.coef + warp * B * Sm::kCoef;
+        if (full && jv2_0 >= 0) pass_a_reg<B, NR, -1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
+        else if (full && jv2_1 < 0) pass_a_reg<B, NR, 1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
+        else pass_a_reg<B, NR, 0>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
+        // raw r (no incoming-trace term) at the outgoing-trace rows, for the Robin trace (R11)
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            const int itr = side ? S.iR_tr : S.iL_tr;
+            if (itr >= cr0 && itr < cr0 + Lw) {
+                const int l = itr - cr0, j = S.first + itr;
+                const double2 rc = __ldg(P.rowc + j);
+                const double u = tile_w[l * kTW + kHalo + lane];
+                const double nb = tile_w[l * kTW + kHalo + lane + ((2 * j - P.nv >= 0) ? -1 : 1)];
+                double f = 0.0;
+                for (int r = 0; r < P.f_rank; ++r) f = fma(P.cf[r] * __ldg(P.fv + r * (P.nv + 1) + j), fx[r], f);
+                sm.rtr[side * kWarp + lane] = fma(rc.x, u, fma(rc.y, nb, f));
+            }
+        }
+        if (full) {
+            kst = pass_b_full<B>(h, q);
+        } else {
+            double kl = 0.0, kl2 = 0.0;
+            kst = pass_b_ragged<B>(h, q, Lw, kl, kl2);
+            if (cr0 + Lw == n) {
+                sm.kb[3 * kWarp + lane] = kl;
+                if (Lw >= 2) sm.kb[2 * kWarp + lane] = kl2;
+            } else if (cr0 + Lw == n - 1) {
+                sm.kb[2 * kWarp + lane] = kl;
+            }
+        }
+        if (cr0 == 0) {
+            sm.kb[0 * kWarp + lane] = h[0];
+            if (Lw >= 2) sm.kb[1 * kWarp + lane] = h[1];
+        } else if (cr0 == 1) {
+            sm.kb[1 * kWarp + lane] = h[0];
+        }
+    }
+    sm.he[warp * kWarp + lane] = hend;
+    sm.ks[warp * kWarp + lane] = kst;
+    __syncthreads();
+
+    // ---- chunk carries with zero block carries, closed form (every warp its own):
+    //      Y0_w = sum_{w'<w} q^{s_w - e_w'} he_w',  Z0_w = ks_w + kap(0, L_w) Y0_w
+    double Y0 = 0.0;
+    for (int c = 0; c < warp; ++c) {
+        const int ec = min(c * L + L, Rb);
+        if (ec > c * L) Y0 = fma(sm.qp[s_w - ec], sm.he[c * kWarp + lane], Y0);
+    }
+    if (Lw > 0) sm.Z0[warp * kWarp + lane] = fma(kap_s(sm.qp, sm.s2, 0, Lw), Y0, kst);
+    __syncthreads();
+    //      X0_w = sum_{w'>w} q^{s_w' - e_w} Z0_w'
+    double X0 = 0.0;
+    for (int c = warp + 1; c < kFusedWarps; ++c) {
+        if (c * L >= Rb) break;
+        X0 = fma(sm.qp[c * L - e_w], sm.Z0[c * kWarp + lane], X0);
+    }
+    // block aggregates F = y at the block's last row, G = x at its first row (zero block carries)
+    if (warp == 0) {
+        double F = 0.0, G = 0.0;
+        for (int c = 0; c < kFusedWarps; ++c) {
+            if (c * L >= Rb) break;
+            const int ec = min(c * L + L, Rb);
+            F = fma(sm.qp[Rb - ec], sm.he[c * kWarp + lane], F);
+            G = fma(sm.qp[c * L], sm.Z0[c * kWarp + lane], G);
+        }
+        sm.pub[0 * kWarp + lane] = F;
+        sm.pub[1 * kWarp + lane] = G;
+    }
+    // boundary rows of the column held by this chunk: x with zero block carries
+    if (Lw > 0) {
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            const int row = (qq < 2) ? qq : n - 4 + qq;
+            const int l = row - cr0;
+            if (row >= 0 && l >= 0 && l < Lw)
+                sm.pub[(2 + qq) * kWarp + lane] =
+                    sm.kb[qq * kWarp + lane] + kap_s(sm.qp, sm.s2, l, Lw) * Y0 + sm.qp[Lw - l] * X0;
+        }
+    }
+    cluster_arrive();
+    cluster_wait();  // every block's pub[] is visible
+
+    // ---- level 2 (warp 0): the block carries Y_blk, X_blk of this block
+    if (warp == 0) {
+        double F[kMaxFusedCluster], G[kMaxFusedCluster], A[4];
+#pragma unroll
+        for (int c = 0; c < kMaxFusedCluster; ++c) {
+            F[c] = (c < nblk) ? ld_dsmem(&sm.pub[0 * kWarp + lane], c) : 0.0;
+            G[c] = (c < nblk) ? ld_dsmem(&sm.pub[1 * kWarp + lane], c) : 0.0;
+        }
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            const int row = (qq < 2) ? qq : n - 4 + qq;
+            A[qq] = ld_dsmem(&sm.pub[(2 + qq) * kWarp + lane], row / R);
+        }
+        // incoming traces enter as column carries: weight*g at row 0 == y_{-1} += weight g / a,
+        // at row n-1 == x_n += weight g / a
+        const double Yt0 = S.injL * sm.gin[lane] / P.a, Xb0 = S.injR * sm.gin[kWarp + lane] / P.a;
+        // chain over the blocks with (Yt0, Xb0): Y_blk(c) forward, X_blk(c) backward
+        double Yb[kMaxFusedCluster], Xb[kMaxFusedCluster];
+        double Y = Yt0;
+#pragma unroll
+        for (int c = 0; c < kMaxFusedCluster; ++c) {
+            Yb[c] = Y;
+            if (c < nblk) Y = fma(P.qp[min(R, n - c * R)], Y, F[c]);
+        }
+        double X = Xb0;
+#pragma unroll
+        for (int c = kMaxFusedCluster - 1; c >= 0; --c) {
+            Xb[c] = X;
+            if (c < nblk) {
+                const int Rc = min(R, n - c * R);
+                X = fma(P.qp[Rc], X, fma(kap_s(P.qp, P.s2, 0, Rc), Yb[c], G[c]));
+            }
+        }
+        // x~ at rows 0, 1, n-2, n-1, then the Woodbury boundary terms
+        double xt[4];
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            const int row = (qq < 2) ? qq : n - 4 + qq;
+            const int c = row / R, l = row - c * R, Rc = min(R, n - c * R);
+            double yc = 0.0, xc = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < kMaxFusedCluster; ++cc)
+                if (cc == c) {
+                    yc = Yb[cc];
+                    xc = Xb[cc];
+                }
+            xt[qq] = A[qq] + kap_s(P.qp, P.s2, l, Rc) * yc + P.qp[Rc - l] * xc;
+        }
+        const double s0 = S.wt0 * xt[0] + S.wt1 * xt[1];
+        const double s1 = S.wb0 * xt[2] + S.wb1 * xt[3];
+        const double dY = -(S.Mi00 * s0 + S.Mi01 * s1) / P.a;  // correction of the top carry
+        const double dX = -(S.Mi10 * s0 + S.Mi11 * s1) / P.a;  // correction of the bottom carry
+        double Ym = 0.0, Xm = 0.0;
+#pragma unroll
+        for (int cc = 0; cc < kMaxFusedCluster; ++cc)
+            if (cc == blk) {
+                Ym = Yb[cc];
+                Xm = Xb[cc];
+            }
+        // responses of this block's carries to the corrections: y_{rb0-1} += q^{rb0} dY;
+        // x_{rb0+Rb} += kap(rb0+Rb, n) dY + q^{n-rb0-Rb} dX
+        const int eb = rb0 + Rb;
+        sm.cb[lane] = fma(P.qp[rb0], dY, Ym);
+        sm.cb[kWarp + lane] = fma(P.qp[n - eb], dX, fma(kap_s(P.qp, P.s2, eb, n), dY, Xm));
+        // Dirichlet ends: the end node value is the incoming trace
+        if (blk == 0 && active && S.ltype == END_DIRI) {
+            const double g = sm.gin[lane];
+            if (S.iL_tr == -1) S.sendL[P.par_out][goff] = g;  // no overlap: the end node is the trace node
+            if (S.ifL >= 0) eif = fmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + m]));
+            if (P.last) {
+                et = fmax(et, fabs(g - P.UT[static_cast<size_t>(S.lo) * P.nx + m]));
+                unew_slab[m] = g;
+            }
+        } else if (blk == 0 && active && S.ltype == END_PHYS && P.last) {
+            unew_slab[m] = 0.0;
+        }
+        if (blk == nblk - 1 && active && S.rtype == END_DIRI) {
+            const double g = sm.gin[kWarp + lane];
+            if (S.iR_tr == n) S.sendR[P.par_out][goff] = g;
+            if (S.ifR >= 0) eif = fmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + m]));
+            if (P.last) {
+                et = fmax(et, fabs(g - P.UT[static_cast<size_t>(S.hi) * P.nx + m]));
+                unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + m] = g;
+            }
+        } else if (blk == nblk - 1 && active && S.rtype == END_PHYS && P.last) {
+            unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + m] = 0.0;
+        }
+    }
+    cluster_arrive();  // this CTA's DSMEM reads are complete (peers may leave after the final wait)
+    __syncthreads();
+
+    // ---- pass C: x = k + kap Y + rho X with this chunk's carries; store u^{n+1}
+    if (Lw > 0) {
+        const double Yb = sm.cb[lane], Xb = sm.cb[kWarp + lane];
+        const double Y = fma(sm.qp[s_w], Yb, Y0);
+        const double X = fma(sm.qp[Rb - e_w], Xb, fma(kap_s(sm.qp, sm.s2, e_w, Rb), Yb, X0));
+        double *dst = unew + static_cast<size_t>(cr0) * P.nx + m;
+        const size_t pitch = P.nx;
+        if (Lw == B) {
+#pragma unroll
+            for (int l = 0; l < B; ++l) {
+                const double x = fma(kap_s(sm.qp, sm.s2, l, B), Y, fma(sm.qp[B - l], X, h[l]));
+                h[l] = x;
+                if (active) dst[l * pitch] = x;
+                tile_w[l * kTW + kHalo + lane] = x;
+            }
+        } else {
+#pragma unroll
+            for (int l = 0; l < B; ++l) {
+                if (l < Lw) {
+                    const double x = fma(kap_s(sm.qp, sm.s2, l, Lw), Y, fma(sm.qp[Lw - l], X, h[l]));
+                    h[l] = x;
+                    if (active) dst[l * pitch] = x;
+                    tile_w[l * kTW + kHalo + lane] = x;
+                }
+            }
+        }
+        if (P.last && active) {  // error at T on every unknown row (a 1/N_t fraction of the steps)
+            const double *ut = P.UT + static_cast<size_t>(S.first + cr0) * P.nx + m;
+#pragma unroll
+            for (int l = 0; l < B; ++l)
+                if (l < Lw) et = fmax(et, fabs(h[l] - ut[l * pitch]));
+        }
+    }
+    grid_dep_launch();  // the next step may start its prologue
+    __syncthreads();
+
+    // ---- special rows of this block, read back from the tile
+    if (warp == 0 && blk < nblk) {
+        auto xrow = [&](int i) {
+            const int li = i - rb0;
+            return sm.tile[(li / L) * Sm::kSlot + (li % L) * kTW + kHalo + lane];
+        };
+        auto inblk = [&](int i) { return i >= rb0 && i < rb0 + Rb; };
+        const double inv_h = 1.0 / P.hv, half_h_dt = 0.5 * P.hv / P.dt;
+        if (active && S.iL_tr >= 0 && inblk(S.iL_tr)) {  // (p + d_v) u at hi_{s-1}, half-cell flux on [c, c+h/2]
+            const double uc = xrow(S.iL_tr);
+            double g = uc;
+            if (P.send_robin) g = P.p * uc - ((uc - xrow(S.iL_tr + 1)) * inv_h + half_h_dt * (uc - sm.rtr[lane]));
+            S.sendL[P.par_out][goff] = g;
+        }
+        if (active && S.iR_tr >= 0 && S.iR_tr < n && inblk(S.iR_tr)) {  // (p - d_v) u at lo_{s+1}, flux on [c-h/2, c]
+            const double uc = xrow(S.iR_tr);
+            double g = uc;
+            if (P.send_robin) g = P.p * uc - ((uc - xrow(S.iR_tr - 1)) * inv_h + half_h_dt * (uc - sm.rtr[kWarp + lane]));
+            S.sendR[P.par_out][goff] = g;
+        }
+        if (active && S.ltype == END_ROBIN && S.ifL >= 0 && inblk(0))
+            eif = fmax(eif, fabs(xrow(0) - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + m]));
+        if (active && S.rtype == END_ROBIN && S.ifR >= 0 && inblk(n - 1))
+            eif = fmax(eif, fabs(xrow(n - 1) - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + m]));
+        if (P.record && active)
+            for (int i = 0; i < FP.nrec; ++i) {
+                const int row = FP.rec_rows[i];
+                if (inblk(row)) P.rec[(static_cast<size_t>(i) * P.nt + P.n) * P.nx + m] = xrow(row);
+            }
+    }
+    // ---- errors: block max, one atomic per CTA
+    if (P.errIF || P.errT) {
+        eif = warp_max(eif);
+        et = warp_max(et);
+        if (lane == 0) {
+            sm.red[warp] = eif;
+            sm.red[kFusedWarps + warp] = et;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double a = 0.0, b = 0.0;
+            for (int c = 0; c < kFusedWarps; ++c) {
+                a = fmax(a, sm.red[c]);
+                b = fmax(b, sm.red[kFusedWarps + c]);
+            }
+            if (a > 0.0 && P.errIF) atomic_max_pos(P.errIF, a);
+            if (b > 0.0 && P.errT) atomic_max_pos(P.errT, b);
+        }
+    }
+    cluster_wait();  // keep pub[] alive until every peer has read it
+}
+
+}  // namespace kfp

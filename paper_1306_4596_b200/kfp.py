@@ -13,7 +13,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkfp.so")
+LIB_PATH = os.environ.get("KFP_LIB_PATH") or os.path.join(_HERE, "libkfp.so")  # override: debugging builds only
 
 KFP_OK, KFP_E_INVAL, KFP_E_CFL, KFP_E_NOMEM, KFP_E_CUDA, KFP_E_STATE = 0, -1, -2, -3, -4, -6
 KIND = {"dirichlet": 0, "robin": 1}
