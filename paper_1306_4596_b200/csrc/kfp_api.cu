@@ -76,12 +76,21 @@ bool fused_kernel(int B, int NR, FusedKernel *k, size_t *smem) {
 // Fused path: P = 16 warps per CTA, chunks of L rows (target 17), row blocks of
 // R = 16 L rows, C = ceil(n_max / R) <= 8 CTAs per cluster.  Otherwise the
 // three-phase path (P = 8, b = 32, block aggregates through global memory).
-Plan make_plan(int n_max, int f_rank, bool allow_fused) {
+Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused) {
     Plan pl;
+    FusedKernel k_unused;
     const int P = kfp::kFusedWarps;
+    const int n_max = *std::max_element(ns.begin(), ns.end());
     int C = (n_max + P * 17 - 1) / (P * 17);
     if (C > 8) C = 8;
-    const int L = (n_max + P * C - 1) / (P * C);
+    int L = (n_max + P * C - 1) / (P * C);
+    // the column's first and last row blocks must hold >= 2 rows (boundary rows 0,1 / n-2,n-1)
+    for (bool ok = false; !ok && L <= 32; ) {
+        ok = true;
+        for (int n : ns)
+            if (n % (P * L) == 1) ok = false;
+        if (!ok) ++L;
+    }
     int B = 0;
     for (int bb : kBs)
         if (bb >= L) {
@@ -97,8 +106,6 @@ Plan make_plan(int n_max, int f_rank, bool allow_fused) {
         pl.NR = (f_rank <= 2) ? 2 : 4;
         pl.b = L;
         pl.R = P * L;
-        FusedKernel k;
-        fused_kernel(pl.B, pl.NR, &k, &pl.smem);
     } else {
         pl.fused = false;
         pl.P = 8;
@@ -177,6 +184,7 @@ struct kfp_problem_s {
     Plan plan;
     double *d_blkagg = nullptr, *d_chkagg = nullptr, *d_carry = nullptr;
     CUtensorMap *d_tmaps = nullptr;  // [nloc][2]
+    double *d_l2c = nullptr;         // [nloc][kL2C]
     std::vector<double *> swr_allocs;
     double *edge_sendL[2] = {nullptr, nullptr}, *edge_recvL[2] = {nullptr, nullptr};
     double *edge_sendR[2] = {nullptr, nullptr}, *edge_recvR[2] = {nullptr, nullptr};
@@ -212,6 +220,8 @@ void free_swr(kfp_problem pb) {
     pb->d_blkagg = pb->d_chkagg = pb->d_carry = nullptr;
     if (pb->d_tmaps) cudaFree(pb->d_tmaps);
     pb->d_tmaps = nullptr;
+    if (pb->d_l2c) cudaFree(pb->d_l2c);
+    pb->d_l2c = nullptr;
     for (int q = 0; q < 2; ++q) pb->edge_sendL[q] = pb->edge_recvL[q] = pb->edge_sendR[q] = pb->edge_recvR[q] = nullptr;
     pb->setup = false;
 }
@@ -333,7 +343,7 @@ StepParams base_params(kfp_problem pb) {
 
 // One time step of every subdomain in P.subs (nsub entries).
 kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, int n, const CUtensorMap *tmaps,
-                       int nrec = 0, const int *rec_rows = nullptr) {
+                       const double *l2c, int nrec = 0, const int *rec_rows = nullptr) {
     P.n = n;
     P.from_u0 = (n == 0);
     for (int r = 0; r < kfp::kMaxRank; ++r) P.cf[r] = (r < pb->f_rank) ? pb->dt * pb->ft[(size_t)r * (pb->nt + 1) + n + 1] : 0.0;
@@ -350,6 +360,7 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
         FP.L = pl.L;
         FP.nrec = nrec;
         FP.rec_rows = rec_rows;
+        FP.l2c = l2c;
         FusedKernel k;
         size_t smem;
         fused_kernel(pl.B, pl.NR, &k, &smem);
@@ -376,6 +387,49 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
         pb->launches += 3;
     }
     KFP_CUDA(cudaGetLastError());
+    return KFP_OK;
+}
+
+// Level-2 constants of every subdomain (kfp_fused.cuh, kL2C layout), long double.
+kfp_status build_l2c(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, double **out,
+                     std::vector<void *> *owner) {
+    *out = nullptr;
+    if (!pl.fused) return KFP_OK;
+    const long double q = pb->q;
+    auto qp = [&](long double e) { return powl(q, e); };
+    auto s2 = [&](int k) {  // sum_{t<k} q^{2t}
+        long double s = 0, t = 1;
+        for (int i = 0; i < k; ++i) {
+            s += t;
+            t *= q * q;
+        }
+        return s;
+    };
+    auto kap = [&](int r, int len) { return qp(r + 1) * s2(len - r); };
+    std::vector<double> h(subs.size() * kfp::kL2C, 0.0);
+    for (size_t i = 0; i < subs.size(); ++i) {
+        const int n = subs[i].n, R = pl.R;
+        double *c = h.data() + i * kfp::kL2C;
+        for (int b = 0; b < 8 && b * R < n; ++b) {
+            const int Rc = std::min(R, n - b * R), bc = b * R, ec = bc + Rc;
+            c[kfp::L2_QR + b] = (double)qp(Rc);
+            c[kfp::L2_K0 + b] = (double)kap(0, Rc);
+            c[kfp::L2_QB + b] = (double)qp(bc);
+            c[kfp::L2_KB + b] = (double)(ec >= n ? 0.0L : kap(ec, n));
+            c[kfp::L2_QE + b] = (double)qp(n - ec);
+        }
+        const int rows[4] = {0, 1, n - 2, n - 1};
+        for (int qq = 0; qq < 4; ++qq) {
+            const int r = std::max(rows[qq], 0), b = r / R, l = r - b * R, Rc = std::min(R, n - b * R);
+            c[kfp::L2_KQ + qq] = (double)kap(l, Rc);
+            c[kfp::L2_RQ + qq] = (double)qp(Rc - l);
+        }
+    }
+    void *d = nullptr;
+    KFP_CUDA(cudaMalloc(&d, sizeof(double) * h.size()));
+    KFP_CUDA(cudaMemcpy(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    *out = static_cast<double *>(d);
+    if (owner) owner->push_back(d);
     return KFP_OK;
 }
 
@@ -467,7 +521,7 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     sd.slab[0] = pb->d_mono[0];
     sd.slab[1] = pb->d_mono[1];
     woodbury(pb, sd, 0.0);
-    Plan pl = make_plan(sd.n, pb->f_rank, true);
+    Plan pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true);
     sd.nblk = (sd.n + pl.R - 1) / pl.R;
     if (kfp_status st = ensure_qtab(pb, std::max(pl.R, sd.n) + 2)) return st;
     if (kfp_status st = configure_kernels(pl)) return st;
@@ -487,14 +541,16 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     std::vector<int> rec_rows(lines.size());
     for (size_t i = 0; i < lines.size(); ++i) rec_rows[i] = lines[i] - sd.first;
     kfp_status st = alloc_general_scratch(pb, pl, 1, &P.blkagg, &P.chkagg, &P.carry, tmp);
+    double *d_l2c = nullptr;
     if (!st) st = build_tmaps(pb, pl, std::vector<SubDev>{sd}, &d_maps, &tmp2);
+    if (!st) st = build_l2c(pb, pl, std::vector<SubDev>{sd}, &d_l2c, &tmp2);
     if (!st && !rec_rows.empty()) {
         if (cudaMalloc(&d_rec, sizeof(int) * rec_rows.size()) != cudaSuccess ||
             cudaMemcpy(d_rec, rec_rows.data(), sizeof(int) * rec_rows.size(), cudaMemcpyHostToDevice) != cudaSuccess)
             st = KFP_E_CUDA;
     }
     for (int n = 0; st == KFP_OK && n < pb->nt; ++n)
-        st = launch_step(pb, pl, P, 1, n, d_maps, (int)rec_rows.size(), d_rec);
+        st = launch_step(pb, pl, P, 1, n, d_maps, d_l2c, (int)rec_rows.size(), d_rec);
     cudaError_t e = cudaStreamSynchronize(pb->stream);
     cudaFree(d_sd);
     if (d_rec) cudaFree(d_rec);
@@ -750,7 +806,9 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
         woodbury(pb, sd, p);
         n_max = std::max(n_max, sd.n);
     }
-    pb->plan = make_plan(n_max, pb->f_rank, true);
+    std::vector<int> ns;
+    for (const SubDev &sd : pb->subs) ns.push_back(sd.n);
+    pb->plan = make_plan(ns, pb->f_rank, true);
     const Plan &pl = pb->plan;
     // the rows of each outgoing trace stencil must sit in one row block
     for (int i = 0; i < nloc; ++i) {
@@ -828,6 +886,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
     }
     KFP_CUDA(cudaMemcpy(pb->d_subs, pb->subs.data(), sizeof(SubDev) * nloc, cudaMemcpyHostToDevice));
     if (kfp_status st = build_tmaps(pb, pl, pb->subs, &pb->d_tmaps, nullptr)) return st;
+    if (kfp_status st = build_l2c(pb, pl, pb->subs, &pb->d_l2c, nullptr)) return st;
     if (kfp_status st = alloc_general_scratch(pb, pl, nloc, &pb->d_blkagg, &pb->d_chkagg, &pb->d_carry, pb->swr_allocs))
         return st;
     pb->setup = true;
@@ -889,7 +948,7 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
         KFP_CUDA(cudaEventRecord(pb->ev[2 + 2 * it], pb->stream));
         for (int n = 0; n < pb->nt; ++n) {
             P.last = (n + 1 == pb->nt);
-            if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n, pb->d_tmaps)) return st;
+            if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n, pb->d_tmaps, pb->d_l2c)) return st;
         }
         KFP_CUDA(cudaEventRecord(pb->ev[3 + 2 * it], pb->stream));
         pb->k_done = k;

@@ -40,7 +40,13 @@ struct FusedParams {
     int L;                        // chunk length (rows per warp), R = P*L rows per CTA
     int nrec;                     // monodomain line recording: number of recorded rows
     const int *rec_rows;          // [nrec] unknown-row index of each recorded line (in line order)
+    const double *l2c;            // [nsub][kL2C] level-2 constants per subdomain (host-computed, see kfp_api.cu)
 };
+// level-2 constants of one subdomain (doubles): for block c < 8: q^{R_c}, kap(0,R_c), q^{b_c},
+// kap_col(e_c), q^{n-e_c} (b_c = c R, e_c = b_c + R_c, kap_col(r) = q^{r+1} s2(n-r)); for the
+// boundary rows 0,1,n-2,n-1: kap(l, R_c), q^{R_c - l} of their block.
+constexpr int kL2C = 5 * 8 + 8;
+enum : int { L2_QR = 0, L2_K0 = 8, L2_QB = 16, L2_KB = 24, L2_QE = 32, L2_KQ = 40, L2_RQ = 44 };
 
 // --------------------------------------------------------------------------- PTX
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
@@ -64,6 +70,23 @@ __device__ __forceinline__ double ld_dsmem(const double *local_addr, int rank) {
     return v;
 }
 
+__device__ __forceinline__ uint32_t mapa_u32(const void *local_addr, int rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local_addr)), "r"(rank));
+    return remote;
+}
+// push two doubles into CTA `rank`'s shared memory (same offset as local dst), completing
+// 16 bytes of transaction count on that CTA's mbarrier at the offset of local bar
+__device__ __forceinline__ void st_async_v2(const void *dst, int rank, double a, double b, const uint64_t *bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+                     mapa_u32(dst, rank)),
+                 "d"(a), "d"(b), "r"(mapa_u32(bar, rank))
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+
 // --------------------------------------------------------------------------- smem
 // per-warp tile slot: B rows of kTW doubles, padded to a multiple of 128 B (TMA destination alignment)
 template <int B>
@@ -77,19 +100,26 @@ struct FusedSmem {
     static constexpr int kSlot = slot_doubles<B>();
     static constexpr int kRows = kFusedWarps * B;
     static constexpr int kCoef = 2 + NR;   // c0', c1', g_0' .. g_{NR-1}'
+    static constexpr int kQ = kFusedWarps * B + 2;
     alignas(128) double tile[kFusedWarps * kSlot];
     double coef[kRows * kCoef];
-    double qp[kQtab], s2[kQtab];           // q^k, sum_{t<k} q^{2t}
-    double he[kFusedWarps * kWarp];        // y at the chunk's last row (zero carry)
-    double ks[kFusedWarps * kWarp];        // k at the chunk's first row (zero carry)
-    double Z0[kFusedWarps * kWarp];        // x at the chunk's first row, zero carries below / above the block
+    double qp[kQ], s2[kQ];                 // q^k, sum_{t<k} q^{2t} for k <= R + 1
+    double kr[2 * B];                      // kap(l, L), q^{L-l} of a full chunk (interleaved)
+    double l2c[kL2C];                      // level-2 constants of this subdomain
+    double he[kFusedWarps * kWarp];        // y at the chunk's last row (zero carry); reused as Yb[8][32]
+    double ks[kFusedWarps * kWarp];        // k at the chunk's first row (zero carry); reused as Xb[8][32]
+    double Y0[kFusedWarps * kWarp];        // chunk carries with zero block carries
+    double X0[kFusedWarps * kWarp];
     double kb[4 * kWarp];                  // k at the column's rows 0,1,n-2,n-1 (chunk-local zero carries)
-    double pub[6 * kWarp];                 // F, G, x~_0, x~_1, x~_{n-2}, x~_{n-1} (block-local) for the cluster
+    double pub[6 * kWarp];                 // this block's F, G and boundary values (pushed to the cluster)
+    double2 rFG[kMaxFusedCluster * kWarp]; // received (F, G) of every block of the cluster
+    double2 rA[2 * kWarp];                 // received boundary values: (x~_0, x~_1), (x~_{n-2}, x~_{n-1})
     double cb[2 * kWarp];                  // this block's carries Y_blk, X_blk
     double gin[2 * kWarp];                 // incoming traces at t_{n+1} (lo end, hi end)
     double rtr[2 * kWarp];                 // raw r at the outgoing-trace rows
     double red[2 * kFusedWarps];
-    uint64_t bar[kFusedWarps];
+    uint64_t bar[kFusedWarps];             // TMA completion per warp
+    uint64_t xbar;                         // cluster exchange completion
 };
 
 template <int B, int NR>
@@ -185,19 +215,31 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
     const int e_w = s_w + Lw;                                   // chunk end (block-local, exclusive)
     const int cr0 = rb0 + s_w;                                  // first column row of the chunk
     const int nblk = S.nblk;
+    const bool live = blk < nblk;                               // the block holds rows of the column
     const double q = P.q;
     const CUtensorMap *tmap = FP.tmaps + 2 * sub + (P.n & 1);
     double *unew_slab = S.slab[(P.n + 1) & 1];
     double *unew = unew_slab + static_cast<size_t>(S.first - S.lo) * P.nx;
     double *tile_w = sm.tile + warp * Sm::kSlot;
     const size_t goff = static_cast<size_t>(P.n) * P.nx + m;   // row t_{n+1} of [nt][nx] arrays
+    auto inblk = [&](int i) { return i >= rb0 && i < rb0 + Rb; };
+    // rows that need a look after pass C (outgoing traces, Robin-end interface errors, recorded lines)
+    bool special = false;
+    if (S.iL_tr >= 0) special |= inblk(S.iL_tr) || inblk(S.iL_tr + 1);
+    if (S.iR_tr >= 0 && S.iR_tr < n) special |= inblk(S.iR_tr) || inblk(S.iR_tr - 1);
+    if (S.ltype == END_ROBIN && S.ifL >= 0) special |= inblk(0);
+    if (S.rtype == END_ROBIN && S.ifR >= 0) special |= inblk(n - 1);
+    if (P.record) special = special || live;
+    const bool errs = (P.errIF != nullptr) && (special || P.last || blk == 0 || blk == nblk - 1);
 
     // ---- prologue: constant tables only (overlaps the previous step under PDL)
-    if (lane == 0) {
-        mbar_init(&sm.bar[warp], 1);
-        if (warp == 0) prefetch_tmap(tmap);
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.xbar, 1);
+        prefetch_tmap(tmap);
     }
+    if (lane == 0) mbar_init(&sm.bar[warp], 1);
     fence_mbar_init();
+    cluster_arrive_relaxed();  // every CTA's xbar is initialised before anybody pushes (wait below)
     for (int rr = threadIdx.x; rr < Rb; rr += blockDim.x) {    // per-row coefficients, scaled by q/a
         const int slot = (rr / L) * B + (rr % L);
         const int j = S.first + rb0 + rr;
@@ -208,10 +250,11 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
 #pragma unroll
         for (int r = 0; r < NR; ++r) c[2 + r] = (r < P.f_rank) ? P.qa * P.cf[r] * __ldg(P.fv + r * (P.nv + 1) + j) : 0.0;
     }
-    for (int k = threadIdx.x; k <= R + 1 && k < kQtab; k += blockDim.x) {
+    for (int k = threadIdx.x; k <= R + 1; k += blockDim.x) {
         sm.qp[k] = __ldg(P.qp + k);
         sm.s2[k] = __ldg(P.s2 + k);
     }
+    if (threadIdx.x < kL2C) sm.l2c[threadIdx.x] = __ldg(FP.l2c + sub * kL2C + threadIdx.x);
     double fx[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r) fx[r] = (r < P.f_rank) ? __ldg(P.fx + r * P.nx + m) : 0.0;
@@ -220,10 +263,14 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
         sm.gin[lane] = (S.ltype != END_PHYS) ? S.gL[P.par_in][goff] : 0.0;
         sm.gin[kWarp + lane] = (S.rtype != END_PHYS) ? S.gR[P.par_in][goff] : 0.0;
     }
+    __syncthreads();  // tables ready
+    if (threadIdx.x < 2 * L) {  // kap(l, L), q^{L-l} of a full chunk
+        const int l = threadIdx.x >> 1;
+        sm.kr[threadIdx.x] = (threadIdx.x & 1) ? sm.qp[L - l] : kap_s(sm.qp, sm.s2, l, L);
+    }
 
     // ---- wait for the previous step, then load this warp's chunk with one TMA
     grid_dep_wait();
-    __syncthreads();
     if (Lw > 0 && !P.from_u0 && lane == 0) {
         mbar_expect_tx(&sm.bar[warp], static_cast<uint32_t>(kTW * L * sizeof(double)));
         tma_load_2d(tile_w, tmap, m0 - kHalo, cr0, &sm.bar[warp]);
@@ -247,10 +294,12 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
         } else {
             mbar_wait(&sm.bar[warp], 0);
             // periodic wrap of the halo at the ends of the x range (TMA zero-fills out-of-range columns)
-            const double *src = S.slab[P.n & 1] + static_cast<size_t>(S.first - S.lo + cr0) * P.nx;
-            if (m0 == 0 && lane < Lw) tile_w[lane * kTW + kHalo - 1] = src[static_cast<size_t>(lane) * P.nx + P.nx - 1];
-            if (m0 + w == P.nx && lane < Lw) tile_w[lane * kTW + kHalo + w] = src[static_cast<size_t>(lane) * P.nx];
-            __syncwarp();
+            if (m0 == 0 || m0 + w == P.nx) {
+                const double *src = S.slab[P.n & 1] + static_cast<size_t>(S.first - S.lo + cr0) * P.nx;
+                if (m0 == 0 && lane < Lw) tile_w[lane * kTW + kHalo - 1] = src[static_cast<size_t>(lane) * P.nx + P.nx - 1];
+                if (m0 + w == P.nx && lane < Lw) tile_w[lane * kTW + kHalo + w] = src[static_cast<size_t>(lane) * P.nx];
+                __syncwarp();
+            }
         }
         const int jv2_0 = 2 * (S.first + cr0) - P.nv;          // 2 j - nv of the chunk's first row
         const int jv2_1 = jv2_0 + 2 * (Lw - 1);
@@ -262,17 +311,19 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
         else if (full && jv2_1 < 0) pass_a_reg<B, NR, 1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
         else pass_a_reg<B, NR, 0>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
         // raw r (no incoming-trace term) at the outgoing-trace rows, for the Robin trace (R11)
+        if (special) {
 #pragma unroll
-        for (int side = 0; side < 2; ++side) {
-            const int itr = side ? S.iR_tr : S.iL_tr;
-            if (itr >= cr0 && itr < cr0 + Lw) {
-                const int l = itr - cr0, j = S.first + itr;
-                const double2 rc = __ldg(P.rowc + j);
-                const double u = tile_w[l * kTW + kHalo + lane];
-                const double nb = tile_w[l * kTW + kHalo + lane + ((2 * j - P.nv >= 0) ? -1 : 1)];
-                double f = 0.0;
-                for (int r = 0; r < P.f_rank; ++r) f = fma(P.cf[r] * __ldg(P.fv + r * (P.nv + 1) + j), fx[r], f);
-                sm.rtr[side * kWarp + lane] = fma(rc.x, u, fma(rc.y, nb, f));
+            for (int side = 0; side < 2; ++side) {
+                const int itr = side ? S.iR_tr : S.iL_tr;
+                if (itr >= cr0 && itr < cr0 + Lw) {
+                    const int l = itr - cr0, j = S.first + itr;
+                    const double2 rc = __ldg(P.rowc + j);
+                    const double u = tile_w[l * kTW + kHalo + lane];
+                    const double nb = tile_w[l * kTW + kHalo + lane + ((2 * j - P.nv >= 0) ? -1 : 1)];
+                    double f = 0.0;
+                    for (int r = 0; r < P.f_rank; ++r) f = fma(P.cf[r] * __ldg(P.fv + r * (P.nv + 1) + j), fx[r], f);
+                    sm.rtr[side * kWarp + lane] = fma(rc.x, u, fma(rc.y, nb, f));
+                }
             }
         }
         if (full) {
@@ -298,111 +349,99 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
     sm.ks[warp * kWarp + lane] = kst;
     __syncthreads();
 
-    // ---- chunk carries with zero block carries, closed form (every warp its own):
-    //      Y0_w = sum_{w'<w} q^{s_w - e_w'} he_w',  Z0_w = ks_w + kap(0, L_w) Y0_w
-    double Y0 = 0.0;
-    for (int c = 0; c < warp; ++c) {
-        const int ec = min(c * L + L, Rb);
-        if (ec > c * L) Y0 = fma(sm.qp[s_w - ec], sm.he[c * kWarp + lane], Y0);
+    // ---- level 1, transposed: warp w scans the 16 chunks of columns 2w, 2w+1 (half-warp each,
+    //      lane = chunk) with affine Kogge-Stone scans:  y_out(k) = q^{L_k} y_out(k-1) + he_k,
+    //      x_start(k) = q^{L_k} x_start(k+1) + Z0_k,  Z0_k = ks_k + kap(0, L_k) Y0_k.
+    {
+        const int col = 2 * warp + (lane >> 4), k = lane & 15;
+        const int Lk = max(0, min(L, Rb - k * L));
+        const double Qk = sm.qp[Lk];
+        double A = Qk, Bv = sm.he[k * kWarp + col];
+#pragma unroll
+        for (int d = 1; d < 16; d <<= 1) {
+            const double Au = __shfl_up_sync(0xffffffffu, A, d, 16), Bu = __shfl_up_sync(0xffffffffu, Bv, d, 16);
+            if (k >= d) {
+                Bv = fma(A, Bu, Bv);
+                A *= Au;
+            }
+        }
+        const double F = __shfl_sync(0xffffffffu, Bv, 15, 16);   // y at the block's last row
+        double y0 = __shfl_up_sync(0xffffffffu, Bv, 1, 16);
+        if (k == 0) y0 = 0.0;
+        const double z0 = (Lk > 0) ? fma(kap_s(sm.qp, sm.s2, 0, Lk), y0, sm.ks[k * kWarp + col]) : 0.0;
+        A = Qk;
+        Bv = z0;
+#pragma unroll
+        for (int d = 1; d < 16; d <<= 1) {
+            const double Ad = __shfl_down_sync(0xffffffffu, A, d, 16), Bd = __shfl_down_sync(0xffffffffu, Bv, d, 16);
+            if (k + d < 16) {
+                Bv = fma(A, Bd, Bv);
+                A *= Ad;
+            }
+        }
+        const double G = __shfl_sync(0xffffffffu, Bv, 0, 16);    // x at the block's first row
+        double x0 = __shfl_down_sync(0xffffffffu, Bv, 1, 16);
+        if (k == 15) x0 = 0.0;
+        sm.Y0[k * kWarp + col] = y0;
+        sm.X0[k * kWarp + col] = x0;
+        if (k == 0) {
+            sm.pub[0 * kWarp + col] = F;
+            sm.pub[1 * kWarp + col] = G;
+        }
+        // column boundary rows held by chunk k of this block: x with zero block carries
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            const int row = (qq < 2) ? qq : n - 4 + qq;
+            const int l = row - rb0 - k * L;
+            if (row >= 0 && l >= 0 && l < Lk)
+                sm.pub[(2 + qq) * kWarp + col] = sm.kb[qq * kWarp + col] + kap_s(sm.qp, sm.s2, l, Lk) * y0 + sm.qp[Lk - l] * x0;
+        }
     }
-    if (Lw > 0) sm.Z0[warp * kWarp + lane] = fma(kap_s(sm.qp, sm.s2, 0, Lw), Y0, kst);
     __syncthreads();
-    //      X0_w = sum_{w'>w} q^{s_w' - e_w} Z0_w'
-    double X0 = 0.0;
-    for (int c = warp + 1; c < kFusedWarps; ++c) {
-        if (c * L >= Rb) break;
-        X0 = fma(sm.qp[c * L - e_w], sm.Z0[c * kWarp + lane], X0);
-    }
-    // block aggregates F = y at the block's last row, G = x at its first row (zero block carries)
-    if (warp == 0) {
-        double F = 0.0, G = 0.0;
-        for (int c = 0; c < kFusedWarps; ++c) {
-            if (c * L >= Rb) break;
-            const int ec = min(c * L + L, Rb);
-            F = fma(sm.qp[Rb - ec], sm.he[c * kWarp + lane], F);
-            G = fma(sm.qp[c * L], sm.Z0[c * kWarp + lane], G);
-        }
-        sm.pub[0 * kWarp + lane] = F;
-        sm.pub[1 * kWarp + lane] = G;
-    }
-    // boundary rows of the column held by this chunk: x with zero block carries
-    if (Lw > 0) {
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-            const int row = (qq < 2) ? qq : n - 4 + qq;
-            const int l = row - cr0;
-            if (row >= 0 && l >= 0 && l < Lw)
-                sm.pub[(2 + qq) * kWarp + lane] =
-                    sm.kb[qq * kWarp + lane] + kap_s(sm.qp, sm.s2, l, Lw) * Y0 + sm.qp[Lw - l] * X0;
-        }
-    }
-    cluster_arrive();
-    cluster_wait();  // every block's pub[] is visible
 
-    // ---- level 2 (warp 0): the block carries Y_blk, X_blk of this block
-    if (warp == 0) {
-        double F[kMaxFusedCluster], G[kMaxFusedCluster], A[4];
-#pragma unroll
-        for (int c = 0; c < kMaxFusedCluster; ++c) {
-            F[c] = (c < nblk) ? ld_dsmem(&sm.pub[0 * kWarp + lane], c) : 0.0;
-            G[c] = (c < nblk) ? ld_dsmem(&sm.pub[1 * kWarp + lane], c) : 0.0;
+    // ---- level 2 (warp 0): push this block's aggregates into every block of the cluster,
+    //      receive everybody's, and resolve the block carries (Woodbury boundary terms and
+    //      incoming-trace injections included).
+    cluster_wait();  // (matches the arrive in the prologue: every xbar is initialised)
+    if (warp == 0 && live) {
+        const int nA = (rb0 <= 1 ? ((rb0 + Rb > 1) ? 1 : 0) : 0) + (inblk(n - 1) || inblk(n - 2) ? 1 : 0);
+        (void)nA;
+        if (lane == 0) mbar_expect_tx(&sm.xbar, static_cast<uint32_t>(nblk * kWarp * 16 + 2 * kWarp * 16));
+        __syncwarp();
+        const double F = sm.pub[lane], G = sm.pub[kWarp + lane];
+        const bool has01 = inblk(0) || inblk(1), hasN = inblk(n - 2) || inblk(n - 1);
+        // rows 0,1 (and n-2,n-1) always sit in the first (last) block: both values come from one block
+        for (int c = 0; c < nblk; ++c) {
+            st_async_v2(&sm.rFG[blk * kWarp + lane], c, F, G, &sm.xbar);
+            if (has01) st_async_v2(&sm.rA[0 * kWarp + lane], c, sm.pub[2 * kWarp + lane], sm.pub[3 * kWarp + lane], &sm.xbar);
+            if (hasN) st_async_v2(&sm.rA[1 * kWarp + lane], c, sm.pub[4 * kWarp + lane], sm.pub[5 * kWarp + lane], &sm.xbar);
         }
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-            const int row = (qq < 2) ? qq : n - 4 + qq;
-            A[qq] = ld_dsmem(&sm.pub[(2 + qq) * kWarp + lane], row / R);
-        }
-        // incoming traces enter as column carries: weight*g at row 0 == y_{-1} += weight g / a,
-        // at row n-1 == x_n += weight g / a
+        mbar_wait(&sm.xbar, 0);
+        const double *l2 = sm.l2c;
+        double *Yb = sm.he, *Xb = sm.ks;  // [c][lane] scratch (he/ks are dead)
         const double Yt0 = S.injL * sm.gin[lane] / P.a, Xb0 = S.injR * sm.gin[kWarp + lane] / P.a;
-        // chain over the blocks with (Yt0, Xb0): Y_blk(c) forward, X_blk(c) backward
-        double Yb[kMaxFusedCluster], Xb[kMaxFusedCluster];
         double Y = Yt0;
-#pragma unroll
-        for (int c = 0; c < kMaxFusedCluster; ++c) {
-            Yb[c] = Y;
-            if (c < nblk) Y = fma(P.qp[min(R, n - c * R)], Y, F[c]);
+        for (int c = 0; c < nblk; ++c) {
+            Yb[c * kWarp + lane] = Y;
+            Y = fma(l2[L2_QR + c], Y, sm.rFG[c * kWarp + lane].x);
         }
         double X = Xb0;
-#pragma unroll
-        for (int c = kMaxFusedCluster - 1; c >= 0; --c) {
-            Xb[c] = X;
-            if (c < nblk) {
-                const int Rc = min(R, n - c * R);
-                X = fma(P.qp[Rc], X, fma(kap_s(P.qp, P.s2, 0, Rc), Yb[c], G[c]));
-            }
+        for (int c = nblk - 1; c >= 0; --c) {
+            Xb[c * kWarp + lane] = X;
+            X = fma(l2[L2_QR + c], X, fma(l2[L2_K0 + c], Yb[c * kWarp + lane], sm.rFG[c * kWarp + lane].y));
         }
-        // x~ at rows 0, 1, n-2, n-1, then the Woodbury boundary terms
-        double xt[4];
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-            const int row = (qq < 2) ? qq : n - 4 + qq;
-            const int c = row / R, l = row - c * R, Rc = min(R, n - c * R);
-            double yc = 0.0, xc = 0.0;
-#pragma unroll
-            for (int cc = 0; cc < kMaxFusedCluster; ++cc)
-                if (cc == c) {
-                    yc = Yb[cc];
-                    xc = Xb[cc];
-                }
-            xt[qq] = A[qq] + kap_s(P.qp, P.s2, l, Rc) * yc + P.qp[Rc - l] * xc;
-        }
-        const double s0 = S.wt0 * xt[0] + S.wt1 * xt[1];
-        const double s1 = S.wb0 * xt[2] + S.wb1 * xt[3];
+        const double2 a01 = sm.rA[lane], aN = sm.rA[kWarp + lane];
+        const int c0 = 0, cN = (n - 1) / R;
+        const double xt0 = a01.x + l2[L2_KQ + 0] * Yb[c0 * kWarp + lane] + l2[L2_RQ + 0] * Xb[c0 * kWarp + lane];
+        const double xt1 = a01.y + l2[L2_KQ + 1] * Yb[c0 * kWarp + lane] + l2[L2_RQ + 1] * Xb[c0 * kWarp + lane];
+        const double xt2 = aN.x + l2[L2_KQ + 2] * Yb[cN * kWarp + lane] + l2[L2_RQ + 2] * Xb[cN * kWarp + lane];
+        const double xt3 = aN.y + l2[L2_KQ + 3] * Yb[cN * kWarp + lane] + l2[L2_RQ + 3] * Xb[cN * kWarp + lane];
+        const double s0 = S.wt0 * xt0 + S.wt1 * xt1;
+        const double s1 = S.wb0 * xt2 + S.wb1 * xt3;
         const double dY = -(S.Mi00 * s0 + S.Mi01 * s1) / P.a;  // correction of the top carry
         const double dX = -(S.Mi10 * s0 + S.Mi11 * s1) / P.a;  // correction of the bottom carry
-        double Ym = 0.0, Xm = 0.0;
-#pragma unroll
-        for (int cc = 0; cc < kMaxFusedCluster; ++cc)
-            if (cc == blk) {
-                Ym = Yb[cc];
-                Xm = Xb[cc];
-            }
-        // responses of this block's carries to the corrections: y_{rb0-1} += q^{rb0} dY;
-        // x_{rb0+Rb} += kap(rb0+Rb, n) dY + q^{n-rb0-Rb} dX
-        const int eb = rb0 + Rb;
-        sm.cb[lane] = fma(P.qp[rb0], dY, Ym);
-        sm.cb[kWarp + lane] = fma(P.qp[n - eb], dX, fma(kap_s(P.qp, P.s2, eb, n), dY, Xm));
+        sm.cb[lane] = fma(l2[L2_QB + blk], dY, Yb[blk * kWarp + lane]);
+        sm.cb[kWarp + lane] = fma(l2[L2_QE + blk], dX, fma(l2[L2_KB + blk], dY, Xb[blk * kWarp + lane]));
         // Dirichlet ends: the end node value is the incoming trace
         if (blk == 0 && active && S.ltype == END_DIRI) {
             const double g = sm.gin[lane];
@@ -427,23 +466,22 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
             unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + m] = 0.0;
         }
     }
-    cluster_arrive();  // this CTA's DSMEM reads are complete (peers may leave after the final wait)
     __syncthreads();
 
     // ---- pass C: x = k + kap Y + rho X with this chunk's carries; store u^{n+1}
     if (Lw > 0) {
         const double Yb = sm.cb[lane], Xb = sm.cb[kWarp + lane];
-        const double Y = fma(sm.qp[s_w], Yb, Y0);
-        const double X = fma(sm.qp[Rb - e_w], Xb, fma(kap_s(sm.qp, sm.s2, e_w, Rb), Yb, X0));
+        const double Y = fma(sm.qp[s_w], Yb, sm.Y0[warp * kWarp + lane]);
+        const double X = fma(sm.qp[Rb - e_w], Xb, fma(kap_s(sm.qp, sm.s2, e_w, Rb), Yb, sm.X0[warp * kWarp + lane]));
         double *dst = unew + static_cast<size_t>(cr0) * P.nx + m;
         const size_t pitch = P.nx;
-        if (Lw == B) {
+        if (Lw == B && L == B) {
 #pragma unroll
             for (int l = 0; l < B; ++l) {
-                const double x = fma(kap_s(sm.qp, sm.s2, l, B), Y, fma(sm.qp[B - l], X, h[l]));
+                const double x = fma(sm.kr[2 * l], Y, fma(sm.kr[2 * l + 1], X, h[l]));
                 h[l] = x;
                 if (active) dst[l * pitch] = x;
-                tile_w[l * kTW + kHalo + lane] = x;
+                if (special) tile_w[l * kTW + kHalo + lane] = x;
             }
         } else {
 #pragma unroll
@@ -452,7 +490,7 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
                     const double x = fma(kap_s(sm.qp, sm.s2, l, Lw), Y, fma(sm.qp[Lw - l], X, h[l]));
                     h[l] = x;
                     if (active) dst[l * pitch] = x;
-                    tile_w[l * kTW + kHalo + lane] = x;
+                    if (special) tile_w[l * kTW + kHalo + lane] = x;
                 }
             }
         }
@@ -464,40 +502,41 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
         }
     }
     grid_dep_launch();  // the next step may start its prologue
-    __syncthreads();
 
     // ---- special rows of this block, read back from the tile
-    if (warp == 0 && blk < nblk) {
-        auto xrow = [&](int i) {
-            const int li = i - rb0;
-            return sm.tile[(li / L) * Sm::kSlot + (li % L) * kTW + kHalo + lane];
-        };
-        auto inblk = [&](int i) { return i >= rb0 && i < rb0 + Rb; };
-        const double inv_h = 1.0 / P.hv, half_h_dt = 0.5 * P.hv / P.dt;
-        if (active && S.iL_tr >= 0 && inblk(S.iL_tr)) {  // (p + d_v) u at hi_{s-1}, half-cell flux on [c, c+h/2]
-            const double uc = xrow(S.iL_tr);
-            double g = uc;
-            if (P.send_robin) g = P.p * uc - ((uc - xrow(S.iL_tr + 1)) * inv_h + half_h_dt * (uc - sm.rtr[lane]));
-            S.sendL[P.par_out][goff] = g;
-        }
-        if (active && S.iR_tr >= 0 && S.iR_tr < n && inblk(S.iR_tr)) {  // (p - d_v) u at lo_{s+1}, flux on [c-h/2, c]
-            const double uc = xrow(S.iR_tr);
-            double g = uc;
-            if (P.send_robin) g = P.p * uc - ((uc - xrow(S.iR_tr - 1)) * inv_h + half_h_dt * (uc - sm.rtr[kWarp + lane]));
-            S.sendR[P.par_out][goff] = g;
-        }
-        if (active && S.ltype == END_ROBIN && S.ifL >= 0 && inblk(0))
-            eif = fmax(eif, fabs(xrow(0) - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + m]));
-        if (active && S.rtype == END_ROBIN && S.ifR >= 0 && inblk(n - 1))
-            eif = fmax(eif, fabs(xrow(n - 1) - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + m]));
-        if (P.record && active)
-            for (int i = 0; i < FP.nrec; ++i) {
-                const int row = FP.rec_rows[i];
-                if (inblk(row)) P.rec[(static_cast<size_t>(i) * P.nt + P.n) * P.nx + m] = xrow(row);
+    if (special) {
+        __syncthreads();
+        if (warp == 0) {
+            auto xrow = [&](int i) {
+                const int li = i - rb0;
+                return sm.tile[(li / L) * Sm::kSlot + (li % L) * kTW + kHalo + lane];
+            };
+            const double inv_h = 1.0 / P.hv, half_h_dt = 0.5 * P.hv / P.dt;
+            if (active && S.iL_tr >= 0 && inblk(S.iL_tr)) {  // (p + d_v) u at hi_{s-1}, half-cell flux on [c, c+h/2]
+                const double uc = xrow(S.iL_tr);
+                double g = uc;
+                if (P.send_robin) g = P.p * uc - ((uc - xrow(S.iL_tr + 1)) * inv_h + half_h_dt * (uc - sm.rtr[lane]));
+                S.sendL[P.par_out][goff] = g;
             }
+            if (active && S.iR_tr >= 0 && S.iR_tr < n && inblk(S.iR_tr)) {  // (p - d_v) u at lo_{s+1}, flux on [c-h/2, c]
+                const double uc = xrow(S.iR_tr);
+                double g = uc;
+                if (P.send_robin) g = P.p * uc - ((uc - xrow(S.iR_tr - 1)) * inv_h + half_h_dt * (uc - sm.rtr[kWarp + lane]));
+                S.sendR[P.par_out][goff] = g;
+            }
+            if (active && S.ltype == END_ROBIN && S.ifL >= 0 && inblk(0))
+                eif = fmax(eif, fabs(xrow(0) - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + m]));
+            if (active && S.rtype == END_ROBIN && S.ifR >= 0 && inblk(n - 1))
+                eif = fmax(eif, fabs(xrow(n - 1) - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + m]));
+            if (P.record && active)
+                for (int i = 0; i < FP.nrec; ++i) {
+                    const int row = FP.rec_rows[i];
+                    if (inblk(row)) P.rec[(static_cast<size_t>(i) * P.nt + P.n) * P.nx + m] = xrow(row);
+                }
+        }
     }
-    // ---- errors: block max, one atomic per CTA
-    if (P.errIF || P.errT) {
+    // ---- errors: block max, one atomic per CTA (only where errors can be non-zero)
+    if (errs) {
         eif = warp_max(eif);
         et = warp_max(et);
         if (lane == 0) {
@@ -511,11 +550,10 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
                 a = fmax(a, sm.red[c]);
                 b = fmax(b, sm.red[kFusedWarps + c]);
             }
-            if (a > 0.0 && P.errIF) atomic_max_pos(P.errIF, a);
+            if (a > 0.0) atomic_max_pos(P.errIF, a);
             if (b > 0.0 && P.errT) atomic_max_pos(P.errT, b);
         }
     }
-    cluster_wait();  // keep pub[] alive until every peer has read it
 }
 
 }  // namespace kfp
