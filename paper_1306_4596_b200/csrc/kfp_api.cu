@@ -55,6 +55,11 @@ struct Plan {
     std::string text;
 };
 
+struct FusedData {
+    CUtensorMap *maps = nullptr;  // [2][nsub][2]: load maps then store maps
+    double *l2c = nullptr, *coefT = nullptr, *tabs = nullptr;
+};
+
 using FusedKernel = void (*)(const kfp::FusedParams);
 constexpr int kBs[] = {8, 16, 17, 24, 32};
 
@@ -137,12 +142,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // Tensor map of a slab's unknown rows: 2-D fp64 [n rows][nx], box (32 + 2*halo) x L.
-bool make_tmap(CUtensorMap *map, double *rows_base, int nx, int nrows, int L) {
+bool make_tmap(CUtensorMap *map, double *rows_base, int nx, int nrows, int L, int box_w = kfp::kTW) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)nx, (cuuint64_t)nrows};
     cuuint64_t strides[1] = {(cuuint64_t)nx * sizeof(double)};
-    cuuint32_t box[2] = {(cuuint32_t)kfp::kTW, (cuuint32_t)L};
+    cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)L};
     cuuint32_t es[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, rows_base, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -158,6 +163,7 @@ struct kfp_problem_s {
     double vmax = 0, T = 0, hx = 0, hv = 0, dt = 0, a = 0, q = 0;
     int f_rank = 0, u0_rank = 0;
     std::vector<double> ft;  // host [f_rank][nt+1]
+    std::vector<double> fv_host;  // host [f_rank][nv+1]
     double *d_fv = nullptr, *d_fx = nullptr, *d_u0v = nullptr, *d_u0x = nullptr;
     double2 *d_rowc = nullptr;
     double *d_qp = nullptr, *d_s2 = nullptr;
@@ -183,8 +189,7 @@ struct kfp_problem_s {
     unsigned long long *d_errT = nullptr, *d_errIF = nullptr;
     Plan plan;
     double *d_blkagg = nullptr, *d_chkagg = nullptr, *d_carry = nullptr;
-    CUtensorMap *d_tmaps = nullptr;  // [nloc][2]
-    double *d_l2c = nullptr;         // [nloc][kL2C]
+    FusedData fd;                    // fused-kernel tensor maps and tables of the SWR setup
     std::vector<double *> swr_allocs;
     double *edge_sendL[2] = {nullptr, nullptr}, *edge_recvL[2] = {nullptr, nullptr};
     double *edge_sendR[2] = {nullptr, nullptr}, *edge_recvR[2] = {nullptr, nullptr};
@@ -218,10 +223,7 @@ void free_swr(kfp_problem pb) {
     if (pb->d_errIF) cudaFree(pb->d_errIF);
     pb->d_errT = pb->d_errIF = nullptr;
     pb->d_blkagg = pb->d_chkagg = pb->d_carry = nullptr;
-    if (pb->d_tmaps) cudaFree(pb->d_tmaps);
-    pb->d_tmaps = nullptr;
-    if (pb->d_l2c) cudaFree(pb->d_l2c);
-    pb->d_l2c = nullptr;
+    pb->fd = FusedData();
     for (int q = 0; q < 2; ++q) pb->edge_sendL[q] = pb->edge_recvL[q] = pb->edge_sendR[q] = pb->edge_recvR[q] = nullptr;
     pb->setup = false;
 }
@@ -342,8 +344,8 @@ StepParams base_params(kfp_problem pb) {
 }
 
 // One time step of every subdomain in P.subs (nsub entries).
-kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, int n, const CUtensorMap *tmaps,
-                       const double *l2c, int nrec = 0, const int *rec_rows = nullptr) {
+kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, int n, const FusedData &fd,
+                       int nrec = 0, const int *rec_rows = nullptr) {
     P.n = n;
     P.from_u0 = (n == 0);
     for (int r = 0; r < kfp::kMaxRank; ++r) P.cf[r] = (r < pb->f_rank) ? pb->dt * pb->ft[(size_t)r * (pb->nt + 1) + n + 1] : 0.0;
@@ -356,11 +358,14 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
     if (pl.fused) {
         kfp::FusedParams FP;
         FP.S = P;
-        FP.tmaps = tmaps;
+        FP.tmaps = fd.maps;
+        FP.smaps = fd.maps + 2 * nsub;
         FP.L = pl.L;
         FP.nrec = nrec;
         FP.rec_rows = rec_rows;
-        FP.l2c = l2c;
+        FP.l2c = fd.l2c;
+        FP.coefT = fd.coefT;
+        FP.tabs = fd.tabs;
         FusedKernel k;
         size_t smem;
         fused_kernel(pl.B, pl.NR, &k, &smem);
@@ -433,16 +438,63 @@ kfp_status build_l2c(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &
     return KFP_OK;
 }
 
+// Per-node coefficient rows (q/a)(1-|nu_j|), (q/a)|nu_j|, (q/a) fv_r(j) (NR columns) and the
+// per-plan table qp[kQ] | s2[kQ] | kr[2B] of the fused kernel.
+kfp_status build_fused_tables(kfp_problem pb, const Plan &pl, std::vector<double> *fv_host, double **coefT,
+                              double **tabs, std::vector<void *> *owner) {
+    *coefT = *tabs = nullptr;
+    if (!pl.fused) return KFP_OK;
+    const int kc = 2 + pl.NR, nn = pb->nv + 1;
+    const long double qa = (long double)pb->q / pb->a;
+    std::vector<double> c((size_t)nn * kc, 0.0);
+    for (int j = 0; j < nn; ++j) {
+        const double v = -pb->vmax + (double)j * pb->hv;
+        const double nu = std::fabs(v * pb->dt / pb->hx);
+        c[(size_t)j * kc + 0] = (double)(qa * (1.0 - nu));
+        c[(size_t)j * kc + 1] = (double)(qa * nu);
+        for (int r = 0; r < pb->f_rank; ++r) c[(size_t)j * kc + 2 + r] = (double)(qa * (*fv_host)[(size_t)r * nn + j]);
+    }
+    const int kQ = ((kfp::kFusedWarps * pl.B + 2) + 1) / 2 * 2;
+    std::vector<double> t(2 * kQ + 2 * pl.B, 0.0);
+    const long double q = pb->q;
+    long double qq = 1.0L, ss = 0.0L;
+    for (int k = 0; k < kQ; ++k) {
+        t[k] = (double)qq;
+        t[kQ + k] = (double)ss;
+        ss += qq * qq;
+        qq *= q;
+    }
+    for (int l = 0; l < pl.L; ++l) {
+        long double kap = 0.0L;  // kap(l, L) = sum_{i=l}^{L-1} q^{i-l} q^{i+1}
+        for (int i = l; i < pl.L; ++i) kap += powl(q, i - l) * powl(q, i + 1);
+        t[2 * kQ + 2 * l] = (double)kap;
+        t[2 * kQ + 2 * l + 1] = (double)powl(q, pl.L - l);
+    }
+    void *d1 = nullptr, *d2 = nullptr;
+    KFP_CUDA(cudaMalloc(&d1, sizeof(double) * c.size()));
+    KFP_CUDA(cudaMemcpy(d1, c.data(), sizeof(double) * c.size(), cudaMemcpyHostToDevice));
+    KFP_CUDA(cudaMalloc(&d2, sizeof(double) * t.size()));
+    KFP_CUDA(cudaMemcpy(d2, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice));
+    *coefT = static_cast<double *>(d1);
+    *tabs = static_cast<double *>(d2);
+    owner->push_back(d1);
+    owner->push_back(d2);
+    return KFP_OK;
+}
+
 // Tensor maps of the slabs of nsub subdomains (host copy -> device array).
+// Load maps (box 36 x L, incl. halo) then store maps (box 32 x L): [2][nsub][2].
 kfp_status build_tmaps(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, CUtensorMap **out,
                        std::vector<void *> *owner) {
     *out = nullptr;
     if (!pl.fused) return KFP_OK;
-    std::vector<CUtensorMap> maps(2 * subs.size());
-    for (size_t i = 0; i < subs.size(); ++i)
+    const size_t ns = subs.size();
+    std::vector<CUtensorMap> maps(4 * ns);
+    for (size_t i = 0; i < ns; ++i)
         for (int q = 0; q < 2; ++q) {
             double *base = subs[i].slab[q] + (size_t)(subs[i].first - subs[i].lo) * pb->nx;
-            if (!make_tmap(&maps[2 * i + q], base, pb->nx, subs[i].n, pl.L)) {
+            if (!make_tmap(&maps[2 * i + q], base, pb->nx, subs[i].n, pl.L) ||
+                !make_tmap(&maps[2 * ns + 2 * i + q], base, pb->nx, subs[i].n, pl.L, kfp::kWarp)) {
                 set_err("cuTensorMapEncodeTiled failed (nx=%d rows=%d L=%d)", pb->nx, subs[i].n, pl.L);
                 return KFP_E_CUDA;
             }
@@ -536,21 +588,21 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     P.rec = pb->d_Ulines;
     P.last = 0;  // no error accumulation on the reference itself; end rows stay 0 (memset)
     std::vector<void *> tmp2;
-    CUtensorMap *d_maps = nullptr;
+    FusedData fd;
     int *d_rec = nullptr;
     std::vector<int> rec_rows(lines.size());
     for (size_t i = 0; i < lines.size(); ++i) rec_rows[i] = lines[i] - sd.first;
     kfp_status st = alloc_general_scratch(pb, pl, 1, &P.blkagg, &P.chkagg, &P.carry, tmp);
-    double *d_l2c = nullptr;
-    if (!st) st = build_tmaps(pb, pl, std::vector<SubDev>{sd}, &d_maps, &tmp2);
-    if (!st) st = build_l2c(pb, pl, std::vector<SubDev>{sd}, &d_l2c, &tmp2);
+    if (!st) st = build_tmaps(pb, pl, std::vector<SubDev>{sd}, &fd.maps, &tmp2);
+    if (!st) st = build_l2c(pb, pl, std::vector<SubDev>{sd}, &fd.l2c, &tmp2);
+    if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &fd.coefT, &fd.tabs, &tmp2);
     if (!st && !rec_rows.empty()) {
         if (cudaMalloc(&d_rec, sizeof(int) * rec_rows.size()) != cudaSuccess ||
             cudaMemcpy(d_rec, rec_rows.data(), sizeof(int) * rec_rows.size(), cudaMemcpyHostToDevice) != cudaSuccess)
             st = KFP_E_CUDA;
     }
     for (int n = 0; st == KFP_OK && n < pb->nt; ++n)
-        st = launch_step(pb, pl, P, 1, n, d_maps, d_l2c, (int)rec_rows.size(), d_rec);
+        st = launch_step(pb, pl, P, 1, n, fd, (int)rec_rows.size(), d_rec);
     cudaError_t e = cudaStreamSynchronize(pb->stream);
     cudaFree(d_sd);
     if (d_rec) cudaFree(d_rec);
@@ -630,6 +682,7 @@ kfp_status kfp_problem_create(const kfp_problem_desc *d, kfp_problem *out) {
     pb->f_rank = d->f_rank;
     pb->u0_rank = d->u0_rank;
     pb->ft.assign(d->ft, d->ft + (size_t)d->f_rank * (d->nt + 1));
+    pb->fv_host.assign(d->fv, d->fv + (size_t)d->f_rank * (d->nv + 1));
     const size_t nn = (size_t)d->nv + 1;
     std::vector<double2> rowc(nn);
     for (size_t j = 0; j < nn; ++j) {
@@ -885,8 +938,14 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
         pb->d_errIF = static_cast<unsigned long long *>(q);
     }
     KFP_CUDA(cudaMemcpy(pb->d_subs, pb->subs.data(), sizeof(SubDev) * nloc, cudaMemcpyHostToDevice));
-    if (kfp_status st = build_tmaps(pb, pl, pb->subs, &pb->d_tmaps, nullptr)) return st;
-    if (kfp_status st = build_l2c(pb, pl, pb->subs, &pb->d_l2c, nullptr)) return st;
+    {
+        std::vector<void *> own;
+        kfp_status st = build_tmaps(pb, pl, pb->subs, &pb->fd.maps, &own);
+        if (!st) st = build_l2c(pb, pl, pb->subs, &pb->fd.l2c, &own);
+        if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &pb->fd.coefT, &pb->fd.tabs, &own);
+        for (void *q : own) pb->swr_allocs.push_back(static_cast<double *>(q));
+        if (st) return st;
+    }
     if (kfp_status st = alloc_general_scratch(pb, pl, nloc, &pb->d_blkagg, &pb->d_chkagg, &pb->d_carry, pb->swr_allocs))
         return st;
     pb->setup = true;
@@ -948,7 +1007,7 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
         KFP_CUDA(cudaEventRecord(pb->ev[2 + 2 * it], pb->stream));
         for (int n = 0; n < pb->nt; ++n) {
             P.last = (n + 1 == pb->nt);
-            if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n, pb->d_tmaps, pb->d_l2c)) return st;
+            if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n, pb->fd)) return st;
         }
         KFP_CUDA(cudaEventRecord(pb->ev[3 + 2 * it], pb->stream));
         pb->k_done = k;

@@ -41,6 +41,9 @@ struct FusedParams {
     int nrec;                     // monodomain line recording: number of recorded rows
     const int *rec_rows;          // [nrec] unknown-row index of each recorded line (in line order)
     const double *l2c;            // [nsub][kL2C] level-2 constants per subdomain (host-computed, see kfp_api.cu)
+    const CUtensorMap *smaps;     // [nsub][2] store maps (box 32 x L) of the slabs' unknown rows
+    const double *coefT;          // [nv+1][2+NR] per-node (q/a)(1-|nu|), (q/a)|nu|, (q/a) fv_r(j)
+    const double *tabs;           // qp[kQ] | s2[kQ] | kr[2B] for this plan (host-computed)
 };
 // level-2 constants of one subdomain (doubles): for block c < 8: q^{R_c}, kap(0,R_c), q^{b_c},
 // kap_col(e_c), q^{n-e_c} (b_c = c R, e_c = b_c + R_c, kap_col(r) = q^{r+1} s2(n-r)); for the
@@ -56,6 +59,15 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, int x, int y, const void *src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -93,19 +105,23 @@ template <int B>
 constexpr int slot_doubles() {
     return ((B * kTW * 8 + 127) / 128) * 128 / 8;
 }
-constexpr int kQtab = kFusedWarps * 32 + 2;  // q^k and s2(k) for k <= R (R <= P * 32)
+// q^k and s2(k) tables for k <= R + 1 (R <= P B), rounded to an even count (16-B bulk copies)
+template <int B>
+__host__ __device__ constexpr int fused_kq() {
+    return ((kFusedWarps * B + 2) + 1) / 2 * 2;
+}
 
 template <int B, int NR>
 struct FusedSmem {
     static constexpr int kSlot = slot_doubles<B>();
     static constexpr int kRows = kFusedWarps * B;
     static constexpr int kCoef = 2 + NR;   // c0', c1', g_0' .. g_{NR-1}'
-    static constexpr int kQ = kFusedWarps * B + 2;
-    alignas(128) double tile[kFusedWarps * kSlot];
-    double coef[kRows * kCoef];
-    double qp[kQ], s2[kQ];                 // q^k, sum_{t<k} q^{2t} for k <= R + 1
-    double kr[2 * B];                      // kap(l, L), q^{L-l} of a full chunk (interleaved)
-    double l2c[kL2C];                      // level-2 constants of this subdomain
+    static constexpr int kQ = fused_kq<B>();
+    static constexpr int kTab = 2 * kQ + 2 * B;
+    alignas(128) double tile[kFusedWarps * kSlot];  // per warp: u^n rows [L][36], then x rows [L][32] (dense)
+    alignas(16) double coef[kRows * kCoef];         // per warp: its chunk's rows of coefT
+    alignas(16) double tab[kTab];                   // qp[kQ] | s2[kQ] | kr[2B]  (copy of FusedParams::tabs)
+    alignas(16) double l2c[kL2C];                   // level-2 constants of this subdomain
     double he[kFusedWarps * kWarp];        // y at the chunk's last row (zero carry); reused as Yb[8][32]
     double ks[kFusedWarps * kWarp];        // k at the chunk's first row (zero carry); reused as Xb[8][32]
     double Y0[kFusedWarps * kWarp];        // chunk carries with zero block carries
@@ -118,7 +134,8 @@ struct FusedSmem {
     double gin[2 * kWarp];                 // incoming traces at t_{n+1} (lo end, hi end)
     double rtr[2 * kWarp];                 // raw r at the outgoing-trace rows
     double red[2 * kFusedWarps];
-    uint64_t bar[kFusedWarps];             // TMA completion per warp
+    uint64_t bar[kFusedWarps];             // tile (TMA) + coefficient rows, per warp
+    uint64_t tbar;                         // tables
     uint64_t xbar;                         // cluster exchange completion
 };
 
@@ -232,53 +249,46 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
     if (P.record) special = special || live;
     const bool errs = (P.errIF != nullptr) && (special || P.last || blk == 0 || blk == nblk - 1);
 
-    // ---- prologue: constant tables only (overlaps the previous step under PDL)
+    const double *qp = sm.tab, *s2 = sm.tab + Sm::kQ, *kr = sm.tab + 2 * Sm::kQ;
+    double *coef_w = sm.coef + warp * B * Sm::kCoef;
+    const uint32_t coef_bytes = static_cast<uint32_t>(Lw * Sm::kCoef * sizeof(double));
+
+    // ---- prologue (constant data only: overlaps the previous step under PDL)
     if (threadIdx.x == 0) {
         mbar_init(&sm.xbar, 1);
+        mbar_init(&sm.tbar, 1);
         prefetch_tmap(tmap);
     }
     if (lane == 0) mbar_init(&sm.bar[warp], 1);
     fence_mbar_init();
     cluster_arrive_relaxed();  // every CTA's xbar is initialised before anybody pushes (wait below)
-    for (int rr = threadIdx.x; rr < Rb; rr += blockDim.x) {    // per-row coefficients, scaled by q/a
-        const int slot = (rr / L) * B + (rr % L);
-        const int j = S.first + rb0 + rr;
-        const double2 rc = __ldg(P.rowc + j);
-        double *c = sm.coef + slot * Sm::kCoef;
-        c[0] = P.qa * rc.x;
-        c[1] = P.qa * rc.y;
-#pragma unroll
-        for (int r = 0; r < NR; ++r) c[2 + r] = (r < P.f_rank) ? P.qa * P.cf[r] * __ldg(P.fv + r * (P.nv + 1) + j) : 0.0;
+    if (threadIdx.x == 0) {    // q-power tables, pass-C coefficients, level-2 constants
+        mbar_expect_tx(&sm.tbar, static_cast<uint32_t>((Sm::kTab + kL2C) * sizeof(double)));
+        bulk_g2s(sm.tab, FP.tabs, Sm::kTab * sizeof(double), &sm.tbar);
+        bulk_g2s(sm.l2c, FP.l2c + sub * kL2C, kL2C * sizeof(double), &sm.tbar);
     }
-    for (int k = threadIdx.x; k <= R + 1; k += blockDim.x) {
-        sm.qp[k] = __ldg(P.qp + k);
-        sm.s2[k] = __ldg(P.s2 + k);
+    if (lane == 0 && Lw > 0) { // this chunk's per-row coefficients (+ its tile below)
+        const uint32_t tile_bytes = P.from_u0 ? 0u : static_cast<uint32_t>(kTW * L * sizeof(double));
+        mbar_expect_tx(&sm.bar[warp], coef_bytes + tile_bytes);
+        bulk_g2s(coef_w, FP.coefT + static_cast<size_t>(S.first + cr0) * Sm::kCoef, coef_bytes, &sm.bar[warp]);
     }
-    if (threadIdx.x < kL2C) sm.l2c[threadIdx.x] = __ldg(FP.l2c + sub * kL2C + threadIdx.x);
-    double fx[NR];
+    double fx[NR];  // this lane's forcing profile times dt ft_r(t_{n+1})
 #pragma unroll
-    for (int r = 0; r < NR; ++r) fx[r] = (r < P.f_rank) ? __ldg(P.fx + r * P.nx + m) : 0.0;
+    for (int r = 0; r < NR; ++r) fx[r] = (r < P.f_rank) ? P.cf[r] * __ldg(P.fx + r * P.nx + m) : 0.0;
     // incoming traces of this step (written by the previous iteration, complete before this launch chain)
     if (warp == 0) {
         sm.gin[lane] = (S.ltype != END_PHYS) ? S.gL[P.par_in][goff] : 0.0;
         sm.gin[kWarp + lane] = (S.rtype != END_PHYS) ? S.gR[P.par_in][goff] : 0.0;
     }
-    __syncthreads();  // tables ready
-    if (threadIdx.x < 2 * L) {  // kap(l, L), q^{L-l} of a full chunk
-        const int l = threadIdx.x >> 1;
-        sm.kr[threadIdx.x] = (threadIdx.x & 1) ? sm.qp[L - l] : kap_s(sm.qp, sm.s2, l, L);
-    }
 
-    // ---- wait for the previous step, then load this warp's chunk with one TMA
+    // ---- wait for the previous step, then load this warp's chunk of u^n with one TMA
     grid_dep_wait();
-    if (Lw > 0 && !P.from_u0 && lane == 0) {
-        mbar_expect_tx(&sm.bar[warp], static_cast<uint32_t>(kTW * L * sizeof(double)));
-        tma_load_2d(tile_w, tmap, m0 - kHalo, cr0, &sm.bar[warp]);
-    }
+    if (Lw > 0 && !P.from_u0 && lane == 0) tma_load_2d(tile_w, tmap, m0 - kHalo, cr0, &sm.bar[warp]);
 
     double h[B];
     double hend = 0.0, kst = 0.0, eif = 0.0, et = 0.0;
     if (Lw > 0) {
+        mbar_wait(&sm.bar[warp], 0);  // coefficient rows (and the tile unless from u0)
         if (P.from_u0) {  // u^0 from the separable u0 tables (0 B of HBM), incl. the halo columns
             for (int l = 0; l < Lw; ++l) {
                 const int j = S.first + cr0 + l;
@@ -292,7 +302,6 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
             }
             __syncwarp();
         } else {
-            mbar_wait(&sm.bar[warp], 0);
             // periodic wrap of the halo at the ends of the x range (TMA zero-fills out-of-range columns)
             if (m0 == 0 || m0 + w == P.nx) {
                 const double *src = S.slab[P.n & 1] + static_cast<size_t>(S.first - S.lo + cr0) * P.nx;
@@ -306,7 +315,6 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
         // full chunks take the unpredicated paths; the chunk holding the column's
         // last two rows takes the ragged one (it captures their k values)
         const bool full = (Lw == B) && (cr0 + Lw <= n - 2);
-        const double *coef_w = sm.coef + warp * B * Sm::kCoef;
         if (full && jv2_0 >= 0) pass_a_reg<B, NR, -1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
         else if (full && jv2_1 < 0) pass_a_reg<B, NR, 1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
         else pass_a_reg<B, NR, 0>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
@@ -321,7 +329,7 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
                     const double u = tile_w[l * kTW + kHalo + lane];
                     const double nb = tile_w[l * kTW + kHalo + lane + ((2 * j - P.nv >= 0) ? -1 : 1)];
                     double f = 0.0;
-                    for (int r = 0; r < P.f_rank; ++r) f = fma(P.cf[r] * __ldg(P.fv + r * (P.nv + 1) + j), fx[r], f);
+                    for (int r = 0; r < P.f_rank; ++r) f = fma(__ldg(P.fv + r * (P.nv + 1) + j), fx[r], f);  // fx has dt f_t
                     sm.rtr[side * kWarp + lane] = fma(rc.x, u, fma(rc.y, nb, f));
                 }
             }
@@ -347,6 +355,7 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
     }
     sm.he[warp * kWarp + lane] = hend;
     sm.ks[warp * kWarp + lane] = kst;
+    mbar_wait(&sm.tbar, 0);  // q-power tables (long since arrived)
     __syncthreads();
 
     // ---- level 1, transposed: warp w scans the 16 chunks of columns 2w, 2w+1 (half-warp each,
@@ -355,7 +364,7 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
     {
         const int col = 2 * warp + (lane >> 4), k = lane & 15;
         const int Lk = max(0, min(L, Rb - k * L));
-        const double Qk = sm.qp[Lk];
+        const double Qk = qp[Lk];
         double A = Qk, Bv = sm.he[k * kWarp + col];
 #pragma unroll
         for (int d = 1; d < 16; d <<= 1) {
@@ -368,7 +377,7 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
         const double F = __shfl_sync(0xffffffffu, Bv, 15, 16);   // y at the block's last row
         double y0 = __shfl_up_sync(0xffffffffu, Bv, 1, 16);
         if (k == 0) y0 = 0.0;
-        const double z0 = (Lk > 0) ? fma(kap_s(sm.qp, sm.s2, 0, Lk), y0, sm.ks[k * kWarp + col]) : 0.0;
+        const double z0 = (Lk > 0) ? fma(kap_s(qp, s2, 0, Lk), y0, sm.ks[k * kWarp + col]) : 0.0;
         A = Qk;
         Bv = z0;
 #pragma unroll
@@ -394,7 +403,7 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
             const int row = (qq < 2) ? qq : n - 4 + qq;
             const int l = row - rb0 - k * L;
             if (row >= 0 && l >= 0 && l < Lk)
-                sm.pub[(2 + qq) * kWarp + col] = sm.kb[qq * kWarp + col] + kap_s(sm.qp, sm.s2, l, Lk) * y0 + sm.qp[Lk - l] * x0;
+                sm.pub[(2 + qq) * kWarp + col] = sm.kb[qq * kWarp + col] + kap_s(qp, s2, l, Lk) * y0 + qp[Lk - l] * x0;
         }
     }
     __syncthreads();
@@ -468,34 +477,39 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
     }
     __syncthreads();
 
-    // ---- pass C: x = k + kap Y + rho X with this chunk's carries; store u^{n+1}
+    // ---- pass C: x = k + kap Y + rho X with this chunk's carries; x -> dense slot -> TMA store of u^{n+1}
+    double *xs = tile_w;  // [L][32] over the (consumed) u^n rows
     if (Lw > 0) {
         const double Yb = sm.cb[lane], Xb = sm.cb[kWarp + lane];
-        const double Y = fma(sm.qp[s_w], Yb, sm.Y0[warp * kWarp + lane]);
-        const double X = fma(sm.qp[Rb - e_w], Xb, fma(kap_s(sm.qp, sm.s2, e_w, Rb), Yb, sm.X0[warp * kWarp + lane]));
-        double *dst = unew + static_cast<size_t>(cr0) * P.nx + m;
-        const size_t pitch = P.nx;
+        const double Y = fma(qp[s_w], Yb, sm.Y0[warp * kWarp + lane]);
+        const double X = fma(qp[Rb - e_w], Xb, fma(kap_s(qp, s2, e_w, Rb), Yb, sm.X0[warp * kWarp + lane]));
+        __syncwarp();
         if (Lw == B && L == B) {
 #pragma unroll
             for (int l = 0; l < B; ++l) {
-                const double x = fma(sm.kr[2 * l], Y, fma(sm.kr[2 * l + 1], X, h[l]));
+                const double x = fma(kr[2 * l], Y, fma(kr[2 * l + 1], X, h[l]));
                 h[l] = x;
-                if (active) dst[l * pitch] = x;
-                if (special) tile_w[l * kTW + kHalo + lane] = x;
+                xs[l * kWarp + lane] = x;
             }
         } else {
 #pragma unroll
             for (int l = 0; l < B; ++l) {
                 if (l < Lw) {
-                    const double x = fma(kap_s(sm.qp, sm.s2, l, Lw), Y, fma(sm.qp[Lw - l], X, h[l]));
+                    const double x = fma(kap_s(qp, s2, l, Lw), Y, fma(qp[Lw - l], X, h[l]));
                     h[l] = x;
-                    if (active) dst[l * pitch] = x;
-                    if (special) tile_w[l * kTW + kHalo + lane] = x;
+                    xs[l * kWarp + lane] = x;
                 }
             }
         }
+        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA store
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(FP.smaps + 2 * sub + ((P.n + 1) & 1), m0, cr0, xs);
+            bulk_commit();
+        }
         if (P.last && active) {  // error at T on every unknown row (a 1/N_t fraction of the steps)
             const double *ut = P.UT + static_cast<size_t>(S.first + cr0) * P.nx + m;
+            const size_t pitch = P.nx;
 #pragma unroll
             for (int l = 0; l < B; ++l)
                 if (l < Lw) et = fmax(et, fabs(h[l] - ut[l * pitch]));
@@ -509,7 +523,7 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
         if (warp == 0) {
             auto xrow = [&](int i) {
                 const int li = i - rb0;
-                return sm.tile[(li / L) * Sm::kSlot + (li % L) * kTW + kHalo + lane];
+                return sm.tile[(li / L) * Sm::kSlot + (li % L) * kWarp + lane];
             };
             const double inv_h = 1.0 / P.hv, half_h_dt = 0.5 * P.hv / P.dt;
             if (active && S.iL_tr >= 0 && inblk(S.iL_tr)) {  // (p + d_v) u at hi_{s-1}, half-cell flux on [c, c+h/2]
@@ -554,6 +568,7 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 2) step_fused_tma(const F
             if (b > 0.0 && P.errT) atomic_max_pos(P.errT, b);
         }
     }
+    if (lane == 0 && Lw > 0) bulk_wait_read0();  // the slot must outlive the TMA store's read
 }
 
 }  // namespace kfp
