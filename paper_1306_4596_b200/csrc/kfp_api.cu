@@ -51,6 +51,7 @@ struct Plan {
     bool fused = false;  // fused TMA/cluster kernel; else the three-phase path
     int P = 8, b = 32, R = 256, C = 1;
     int L = 0, B = 0, NR = 2;  // fused: chunk rows, register-array size (template), forcing ranks (template)
+    int Gc_total = 1;          // fused: co-resident clusters (persistent grid size over all subdomains)
     size_t smem = 0;
     std::string text;
 };
@@ -61,7 +62,7 @@ struct FusedData {
 };
 
 using FusedKernel = void (*)(const kfp::FusedParams);
-constexpr int kBs[] = {8, 16, 17, 24, 32};
+constexpr int kBs[] = {8, 16, 17, 24, 32, 33};
 
 template <int B, int NR>
 void fused_entry(FusedKernel *k, size_t *smem) {
@@ -72,7 +73,7 @@ bool fused_kernel(int B, int NR, FusedKernel *k, size_t *smem) {
 #define KFP_ENTRY(BB)                                   \
     if (B == BB && NR == 2) { fused_entry<BB, 2>(k, smem); return true; } \
     if (B == BB && NR == 4) { fused_entry<BB, 4>(k, smem); return true; }
-    KFP_ENTRY(8) KFP_ENTRY(16) KFP_ENTRY(17) KFP_ENTRY(24) KFP_ENTRY(32)
+    KFP_ENTRY(8) KFP_ENTRY(16) KFP_ENTRY(17) KFP_ENTRY(24) KFP_ENTRY(32) KFP_ENTRY(33)
 #undef KFP_ENTRY
     return false;
 }
@@ -86,11 +87,12 @@ Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused) {
     FusedKernel k_unused;
     const int P = kfp::kFusedWarps;
     const int n_max = *std::max_element(ns.begin(), ns.end());
-    int C = (n_max + P * 17 - 1) / (P * 17);
-    if (C > 8) C = 8;
+    // the smallest cluster whose CTAs hold at most 33 rows per warp (1 CTA per SM, 128 registers)
+    int C = 1;
+    while (C < 8 && (n_max + P * C - 1) / (P * C) > 33) ++C;
     int L = (n_max + P * C - 1) / (P * C);
     // the column's first and last row blocks must hold >= 2 rows (boundary rows 0,1 / n-2,n-1)
-    for (bool ok = false; !ok && L <= 32; ) {
+    for (bool ok = false; !ok && L <= 33; ) {
         ok = true;
         for (int n : ns)
             if (n % (P * L) == 1) ok = false;
@@ -359,18 +361,19 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
         kfp::FusedParams FP;
         FP.S = P;
         FP.tmaps = fd.maps;
-        FP.smaps = fd.maps + 2 * nsub;
         FP.L = pl.L;
+        FP.ntiles = ntiles;
+        FP.Gc = std::max(1, std::min(ntiles, pl.Gc_total / std::max(1, nsub)));
         FP.nrec = nrec;
         FP.rec_rows = rec_rows;
-        FP.l2c = fd.l2c;
+        FP.l2m = fd.l2c;
         FP.coefT = fd.coefT;
         FP.tabs = fd.tabs;
         FusedKernel k;
         size_t smem;
         fused_kernel(pl.B, pl.NR, &k, &smem);
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(pl.C, ntiles, nsub);
+        cfg.gridDim = dim3(pl.C, FP.Gc, nsub);
         cfg.blockDim = block;
         cfg.dynamicSmemBytes = smem;
         cfg.stream = pb->stream;
@@ -395,12 +398,15 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
     return KFP_OK;
 }
 
-// Level-2 constants of every subdomain (kfp_fused.cuh, kL2C layout), long double.
-kfp_status build_l2c(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, double **out,
+// Level-2 linear maps (kfp_fused.cuh, kL2M layout): for every subdomain and row block
+// `me`, the block carries (Y_blk(me), X_blk(me)) as linear functions of the 22 inputs
+// v = (F_0..7, G_0..7, x~ at rows 0,1,n-2,n-1, g_lo, g_hi), obtained by running the
+// block chain + Woodbury solve on the unit vectors, in long double.
+kfp_status build_l2m(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, double **out,
                      std::vector<void *> *owner) {
     *out = nullptr;
     if (!pl.fused) return KFP_OK;
-    const long double q = pb->q;
+    const long double q = pb->q, a = pb->a;
     auto qp = [&](long double e) { return powl(q, e); };
     auto s2 = [&](int k) {  // sum_{t<k} q^{2t}
         long double s = 0, t = 1;
@@ -411,23 +417,50 @@ kfp_status build_l2c(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &
         return s;
     };
     auto kap = [&](int r, int len) { return qp(r + 1) * s2(len - r); };
-    std::vector<double> h(subs.size() * kfp::kL2C, 0.0);
+    const int C = pl.C, R = pl.R;
+    std::vector<double> h(subs.size() * C * kfp::kL2M, 0.0);
     for (size_t i = 0; i < subs.size(); ++i) {
-        const int n = subs[i].n, R = pl.R;
-        double *c = h.data() + i * kfp::kL2C;
-        for (int b = 0; b < 8 && b * R < n; ++b) {
+        const SubDev &sd = subs[i];
+        const int n = sd.n, nb = sd.nblk;
+        std::vector<long double> QR(nb), K0(nb), QB(nb), KB(nb), QE(nb);
+        for (int b = 0; b < nb; ++b) {
             const int Rc = std::min(R, n - b * R), bc = b * R, ec = bc + Rc;
-            c[kfp::L2_QR + b] = (double)qp(Rc);
-            c[kfp::L2_K0 + b] = (double)kap(0, Rc);
-            c[kfp::L2_QB + b] = (double)qp(bc);
-            c[kfp::L2_KB + b] = (double)(ec >= n ? 0.0L : kap(ec, n));
-            c[kfp::L2_QE + b] = (double)qp(n - ec);
+            QR[b] = qp(Rc);
+            K0[b] = kap(0, Rc);
+            QB[b] = qp(bc);
+            KB[b] = (ec >= n) ? 0.0L : kap(ec, n);
+            QE[b] = qp(n - ec);
         }
         const int rows[4] = {0, 1, n - 2, n - 1};
-        for (int qq = 0; qq < 4; ++qq) {
-            const int r = std::max(rows[qq], 0), b = r / R, l = r - b * R, Rc = std::min(R, n - b * R);
-            c[kfp::L2_KQ + qq] = (double)kap(l, Rc);
-            c[kfp::L2_RQ + qq] = (double)qp(Rc - l);
+        for (int j = 0; j < kfp::kL2N; ++j) {
+            long double v[kfp::kL2N] = {0};
+            v[j] = 1.0L;
+            const long double Yt0 = sd.injL * v[20] / a, Xb0 = sd.injR * v[21] / a;
+            std::vector<long double> Yb(nb), Xb(nb);
+            long double Y = Yt0;
+            for (int b = 0; b < nb; ++b) {
+                Yb[b] = Y;
+                Y = QR[b] * Y + (b < 8 ? v[b] : 0.0L);
+            }
+            long double X = Xb0;
+            for (int b = nb - 1; b >= 0; --b) {
+                Xb[b] = X;
+                X = QR[b] * X + K0[b] * Yb[b] + (b < 8 ? v[8 + b] : 0.0L);
+            }
+            long double xt[4];
+            for (int qq = 0; qq < 4; ++qq) {
+                const int r = std::max(rows[qq], 0), b = r / R, l = r - b * R, Rc = std::min(R, n - b * R);
+                xt[qq] = v[16 + qq] + kap(l, Rc) * Yb[b] + qp(Rc - l) * Xb[b];
+            }
+            const long double s0 = sd.wt0 * xt[0] + (long double)sd.wt1 * xt[1];
+            const long double s1 = sd.wb0 * xt[2] + (long double)sd.wb1 * xt[3];
+            const long double dY = -(sd.Mi00 * s0 + (long double)sd.Mi01 * s1) / a;
+            const long double dX = -(sd.Mi10 * s0 + (long double)sd.Mi11 * s1) / a;
+            for (int me = 0; me < nb; ++me) {
+                double *c = h.data() + (i * C + me) * kfp::kL2M;
+                c[j] = (double)(Yb[me] + QB[me] * dY);
+                c[24 + j] = (double)(Xb[me] + KB[me] * dY + QE[me] * dX);
+            }
         }
     }
     void *d = nullptr;
@@ -507,12 +540,26 @@ kfp_status build_tmaps(kfp_problem pb, const Plan &pl, const std::vector<SubDev>
     return KFP_OK;
 }
 
-kfp_status configure_kernels(const Plan &pl) {
+kfp_status configure_kernels(Plan &pl) {
     if (pl.fused) {
         FusedKernel k;
         size_t smem;
         fused_kernel(pl.B, pl.NR, &k, &smem);
         KFP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(pl.C, 1024, 1);
+        cfg.blockDim = dim3(pl.P * kfp::kWarp);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = pl.C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        KFP_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
+        pl.Gc_total = std::max(1, ncl);
     } else {
         KFP_CUDA(cudaFuncSetAttribute(kfp::step_phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
         KFP_CUDA(cudaFuncSetAttribute(kfp::step_phase3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
@@ -594,7 +641,7 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     for (size_t i = 0; i < lines.size(); ++i) rec_rows[i] = lines[i] - sd.first;
     kfp_status st = alloc_general_scratch(pb, pl, 1, &P.blkagg, &P.chkagg, &P.carry, tmp);
     if (!st) st = build_tmaps(pb, pl, std::vector<SubDev>{sd}, &fd.maps, &tmp2);
-    if (!st) st = build_l2c(pb, pl, std::vector<SubDev>{sd}, &fd.l2c, &tmp2);
+    if (!st) st = build_l2m(pb, pl, std::vector<SubDev>{sd}, &fd.l2c, &tmp2);
     if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &fd.coefT, &fd.tabs, &tmp2);
     if (!st && !rec_rows.empty()) {
         if (cudaMalloc(&d_rec, sizeof(int) * rec_rows.size()) != cudaSuccess ||
@@ -862,7 +909,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
     std::vector<int> ns;
     for (const SubDev &sd : pb->subs) ns.push_back(sd.n);
     pb->plan = make_plan(ns, pb->f_rank, true);
-    const Plan &pl = pb->plan;
+    Plan &pl = pb->plan;
     // the rows of each outgoing trace stencil must sit in one row block
     for (int i = 0; i < nloc; ++i) {
         SubDev &sd = pb->subs[i];
@@ -941,7 +988,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
     {
         std::vector<void *> own;
         kfp_status st = build_tmaps(pb, pl, pb->subs, &pb->fd.maps, &own);
-        if (!st) st = build_l2c(pb, pl, pb->subs, &pb->fd.l2c, &own);
+        if (!st) st = build_l2m(pb, pl, pb->subs, &pb->fd.l2c, &own);
         if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &pb->fd.coefT, &pb->fd.tabs, &own);
         for (void *q : own) pb->swr_allocs.push_back(static_cast<double *>(q));
         if (st) return st;
@@ -1148,6 +1195,34 @@ kfp_status kfp_swr_trace(kfp_problem pb, int32_t i, int32_t dir, double *out) {
 }
 
 int64_t kfp_launch_count(kfp_problem pb) { return pb ? pb->launches : -1; }
+
+#ifdef KFP_TRACE
+// debug builds only (not part of include/kfp.h): one traced step launch of the current setup
+extern "C" int kfp_debug_trace_step(kfp_problem pb, int n, unsigned long long *host, int cap) {
+    unsigned long long *d = nullptr;
+    cudaMalloc(&d, sizeof(unsigned long long) * cap * 8);
+    cudaMemset(d, 0, sizeof(unsigned long long) * cap * 8);
+    cudaMemcpyToSymbol(kfp::g_kfp_trace, &d, sizeof(d));
+    StepParams P = base_params(pb);
+    P.subs = pb->d_subs;
+    P.send_robin = (pb->kind == KFP_ROBIN);
+    P.p = pb->p;
+    P.UT = pb->d_UT;
+    P.Ulines = pb->d_Ulines;
+    P.errT = pb->d_errT;
+    P.errIF = pb->d_errIF;
+    P.par_in = 0;
+    P.par_out = 1;
+    P.last = 0;
+    launch_step(pb, pb->plan, P, (int)pb->subs.size(), n, pb->fd);
+    cudaDeviceSynchronize();
+    unsigned long long *z = nullptr;
+    cudaMemcpyToSymbol(kfp::g_kfp_trace, &z, sizeof(z));
+    cudaMemcpy(host, d, sizeof(unsigned long long) * cap * 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return (int)cudaGetLastError();
+}
+#endif
 
 const char *kfp_plan(kfp_problem pb) {
     if (!pb) return "";
