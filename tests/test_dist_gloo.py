@@ -1,0 +1,141 @@
+"""-m "not gpu": the multi-rank host logic (paper_1306_4596_b200/dist.py) on CPU with gloo, world_size 2.
+
+The distributed driver (block partition, edge-trace exchange by point-to-point
+send/recv after every Jacobi iteration, MAX all-reduce of the error history)
+is run with an oracle-backed local block: each rank owns half of the
+subdomains.  Because the exchange only moves bytes, the result must be
+bitwise identical to the single-process oracle SWR.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import kfp_inputs as ki
+
+RUNS = {
+    "robin4": ki.scaled(ki.config("c3"), nx=16, nv=64, nt=30, K=5).with_(n_sub=4),
+    "dirichlet4": ki.scaled(ki.config("c4"), nx=16, nv=64, nt=30, K=5).with_(n_sub=4, overlap=4),
+}
+
+
+class OracleBlock:
+    """The dist.py local-block interface backed by the CPU oracle (tests only)."""
+
+    def __init__(self, prob, run, rank, world):
+        import oracle
+        from paper_1306_4596_b200.dist import block_of
+
+        self.orc = oracle
+        self.prob, self.run = prob, run
+        g = run.grid
+        self.s_begin, self.s_end = block_of(rank, world, run.n_sub)
+        self.lo, self.hi = oracle.subdomains(g.nv, run.n_sub, run.overlap)
+        S = run.n_sub
+        lines = sorted({int(self.lo[s]) for s in range(1, S)} | {int(self.hi[s]) for s in range(S - 1)})
+        self.UT, rec = oracle.monodomain(prob, lines)
+        self.Uline = {j: rec[i] for i, j in enumerate(lines)}
+        shape = (g.nt, g.nx)
+        self.has_left, self.has_right = self.s_begin > 0, self.s_end < S
+        z = lambda: [torch.zeros(shape, dtype=torch.float64) for _ in range(2)]
+        self.send_left, self.recv_left = (z(), z()) if self.has_left else (None, None)
+        self.send_right, self.recv_right = (z(), z()) if self.has_right else (None, None)
+        # local interfaces: toL[i] (sent by i+1 to i), toR[i] (sent by i to i+1), by parity
+        self.toL = {i: z() for i in range(self.s_begin, self.s_end - 1)}
+        self.toR = {i: z() for i in range(self.s_begin, self.s_end - 1)}
+        self.k = 0
+        self.eT, self.eI = [], []
+        self.uT = {}
+
+    def reset(self):
+        pass
+
+    def iterate(self):
+        o, run = self.orc, self.run
+        self.k += 1
+        pin, pout = (self.k - 1) & 1, self.k & 1
+        S = run.n_sub
+        et = o.END_ROBIN if run.kind == "robin" else o.END_DIRICHLET
+        eT = eI = 0.0
+        for s in range(self.s_begin, self.s_end):
+            lo, hi = int(self.lo[s]), int(self.hi[s])
+            if s == 0:
+                gL = None
+            elif s == self.s_begin:
+                gL = self.recv_left[pin].numpy()
+            else:
+                gL = self.toR[s - 1][pin].numpy()
+            if s == S - 1:
+                gR = None
+            elif s == self.s_end - 1:
+                gR = self.recv_right[pin].numpy()
+            else:
+                gR = self.toL[s][pin].numpy()
+            rec = [n for n in ((lo,) if s > 0 else ()) + ((hi,) if s < S - 1 else ())]
+            uT, sL, sR, r = o.window(self.prob, lo, hi, o.END_PHYS if s == 0 else et, o.END_PHYS if s == S - 1 else et,
+                                     run.p, gL, gR, run.kind, int(self.hi[s - 1]) if s > 0 else -1,
+                                     int(self.lo[s + 1]) if s < S - 1 else -1, rec_nodes=rec)
+            if s > 0:
+                dst = self.send_left[pout] if s == self.s_begin else self.toL[s - 1][pout]
+                dst.copy_(torch.from_numpy(sL))
+            if s < S - 1:
+                dst = self.send_right[pout] if s == self.s_end - 1 else self.toR[s][pout]
+                dst.copy_(torch.from_numpy(sR))
+            for i, node in enumerate(rec):
+                eI = max(eI, float(np.abs(r[i] - self.Uline[node]).max()))
+            eT = max(eT, float(np.abs(uT - self.UT[lo:hi + 1]).max()))
+            self.uT[s] = uT
+        self.eT.append(eT)
+        self.eI.append(eI)
+
+    def history(self):
+        return torch.tensor(self.eT, dtype=torch.float64), torch.tensor(self.eI, dtype=torch.float64)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, name, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1306_4596_b200.dist import run_swr
+
+    run = RUNS[name]
+    blk = OracleBlock(ki.make_problem(run), run, rank, world)
+    eT, eI = run_swr(blk, run.K, rank, world)
+    out[rank] = (eT, eI, {s: blk.uT[s] for s in blk.uT})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", list(RUNS))
+def test_two_rank_gloo_matches_single_process(orc, name):
+    run = RUNS[name]
+    ref = orc.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, run.K)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), name, out), nprocs=2, join=True)
+    for rank in (0, 1):
+        eT, eI, slabs = out[rank]
+        assert np.array_equal(eT, ref["err_T"]) and np.array_equal(eI, ref["err_if"])  # MAX all-reduce is exact
+        for s, a in slabs.items():
+            assert np.array_equal(a, ref["uT_sub"][s]), (rank, s)
+    # both ranks together hold every subdomain
+    assert sorted(list(out[0][2]) + list(out[1][2])) == list(range(run.n_sub))
+
+
+def test_block_partition():
+    from paper_1306_4596_b200.dist import block_of
+
+    assert [block_of(r, 8, 32) for r in range(8)] == [(4 * r, 4 * r + 4) for r in range(8)]
+    with pytest.raises(ValueError):
+        block_of(0, 3, 32)
