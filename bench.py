@@ -89,6 +89,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def committed_traffic(plan: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture of the same plan, or None."""
+    import glob
+
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json"))):
+        try:
+            d = json.load(open(f))
+            if d.get("bench", {}).get("config", {}).get("plan") == plan:
+                best = float(d["dram_traffic_bytes_per_launch"])
+        except Exception:
+            pass
+    return best
+
+
 def default_workload(n_gpus: int) -> str:
     return "c2" if n_gpus == 1 else f"c4w{n_gpus}"
 
@@ -191,8 +206,8 @@ def bench_single(args):
     bytes_per_launch = BYTES_PER_UPDATE * g.nx * unknown_rows
     achieved = bytes_per_launch / per_launch_s / 1e9
     peak, peak_kind = measured_peaks()
+    traffic = committed_traffic(plan := pb.plan())
     eT, eI = pb.history()
-    plan = pb.plan()
 
     # end to end through the public API with host buffers (create -> solve -> read back)
     e2e_steps = max(1, min(args.steps, 2))
@@ -226,7 +241,8 @@ def bench_single(args):
                          (2 * 8 * g.nx * (g.nv + run.n_sub) / 1e6),
                    "parallelism": "v-subdomains on 1 GPU", "updates_per_step": updates},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_kind": peak_kind, "kernel": "kfp::step_fused",
+                     "traffic": traffic, "peak_kind": peak_kind, "kernel": "kfp::step_fused_tma",
+                     "traffic_source": "profiles/*_ncu_summary.json (ncu --set full, same plan)" if traffic else None,
                      "bytes_per_launch": bytes_per_launch, "avg_launch_us": per_launch_s * 1e6},
         "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": pb.h2d_bytes,
                 "d2h_bytes_per_step": int(d2h)},

@@ -113,6 +113,8 @@ Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused) {
         pl.NR = (f_rank <= 2) ? 2 : 4;
         pl.b = L;
         pl.R = P * L;
+        FusedKernel k_unused;
+        fused_kernel(pl.B, pl.NR, &k_unused, &pl.smem);
     } else {
         pl.fused = false;
         pl.P = 8;
