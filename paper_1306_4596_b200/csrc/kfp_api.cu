@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -62,21 +63,25 @@ struct FusedData {
 };
 
 using FusedKernel = void (*)(const kfp::FusedParams);
-constexpr int kBs[] = {8, 16, 17, 24, 32, 33};
-
-template <int B, int NR>
+template <int B, int NR, int P>
 void fused_entry(FusedKernel *k, size_t *smem) {
-    *k = kfp::step_fused_tma<B, NR>;
-    *smem = kfp::fused_smem_bytes<B, NR>();
+    *k = kfp::step_fused_tma<B, NR, P>;
+    *smem = kfp::fused_smem_bytes<B, NR, P>();
 }
-bool fused_kernel(int B, int NR, FusedKernel *k, size_t *smem) {
-#define KFP_ENTRY(BB)                                   \
-    if (B == BB && NR == 2) { fused_entry<BB, 2>(k, smem); return true; } \
-    if (B == BB && NR == 4) { fused_entry<BB, 4>(k, smem); return true; }
-    KFP_ENTRY(8) KFP_ENTRY(16) KFP_ENTRY(17) KFP_ENTRY(24) KFP_ENTRY(32) KFP_ENTRY(33)
+// instantiated (B, NR, P) combinations of the fused kernel
+bool fused_kernel(int B, int NR, int P, FusedKernel *k, size_t *smem) {
+#define KFP_ENTRY(BB, NN, PP)             \
+    if (B == BB && NR == NN && P == PP) { \
+        fused_entry<BB, NN, PP>(k, smem); \
+        return true;                      \
+    }
+    KFP_ENTRY(8, 2, 8) KFP_ENTRY(16, 2, 8) KFP_ENTRY(17, 2, 8) KFP_ENTRY(32, 2, 8) KFP_ENTRY(33, 2, 8)
+    KFP_ENTRY(8, 4, 8) KFP_ENTRY(16, 4, 8) KFP_ENTRY(17, 4, 8) KFP_ENTRY(32, 4, 8) KFP_ENTRY(33, 4, 8)
+    KFP_ENTRY(32, 2, 16) KFP_ENTRY(33, 2, 16)
 #undef KFP_ENTRY
     return false;
 }
+constexpr int kBs[] = {8, 16, 17, 32, 33};
 
 // Launch geometry for columns of at most n_max unknown rows.
 // Fused path: P = 16 warps per CTA, chunks of L rows (target 17), row blocks of
@@ -84,39 +89,44 @@ bool fused_kernel(int B, int NR, FusedKernel *k, size_t *smem) {
 // three-phase path (P = 8, b = 32, block aggregates through global memory).
 Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused) {
     Plan pl;
-    FusedKernel k_unused;
-    const int P = kfp::kFusedWarps;
     const int n_max = *std::max_element(ns.begin(), ns.end());
-    // the smallest cluster whose CTAs hold at most 33 rows per warp (1 CTA per SM, 128 registers)
-    int C = 1;
-    while (C < 8 && (n_max + P * C - 1) / (P * C) > 33) ++C;
-    int L = (n_max + P * C - 1) / (P * C);
-    // the column's first and last row blocks must hold >= 2 rows (boundary rows 0,1 / n-2,n-1)
-    for (bool ok = false; !ok && L <= 33; ) {
-        ok = true;
-        for (int n : ns)
-            if (n % (P * L) == 1) ok = false;
-        if (!ok) ++L;
-    }
-    int B = 0;
-    for (int bb : kBs)
-        if (bb >= L) {
-            B = bb;
+    const int NR = (f_rank <= 2) ? 2 : 4;
+    // P = 8 warps (2 CTAs per SM) first, then P = 16 (1 CTA per SM): the smallest cluster whose
+    // warps hold at most 33 rows; the column's first/last row blocks must hold >= 2 rows.
+    const char *force = getenv("KFP_FORCE_P");  // debugging / experiments only
+    for (int P : {8, 16}) {
+        if (force && atoi(force) != P) continue;
+        int C = 1;
+        while (C < 8 && (n_max + P * C - 1) / (P * C) > 33) ++C;
+        int L = (n_max + P * C - 1) / (P * C);
+        for (bool ok = false; !ok && L <= 33;) {
+            ok = true;
+            for (int n : ns)
+                if (n % (P * L) == 1) ok = false;
+            if (!ok) ++L;
+        }
+        int B = 0;
+        for (int bb : kBs)
+            if (bb >= L) {
+                B = bb;
+                break;
+            }
+        FusedKernel k;
+        size_t smem = 0;
+        if (allow_fused && B > 0 && L <= 33 && f_rank <= kfp::kNRmax && fused_kernel(B, NR, P, &k, &smem)) {
+            pl.fused = true;
+            pl.P = P;
+            pl.C = C;
+            pl.L = L;
+            pl.B = B;
+            pl.NR = NR;
+            pl.b = L;
+            pl.R = P * L;
+            pl.smem = smem;
             break;
         }
-    if (allow_fused && B > 0 && f_rank <= kfp::kNRmax) {
-        pl.fused = true;
-        pl.P = P;
-        pl.C = C;
-        pl.L = L;
-        pl.B = B;
-        pl.NR = (f_rank <= 2) ? 2 : 4;
-        pl.b = L;
-        pl.R = P * L;
-        FusedKernel k_unused;
-        fused_kernel(pl.B, pl.NR, &k_unused, &pl.smem);
-    } else {
-        pl.fused = false;
+    }
+    if (!pl.fused) {
         pl.P = 8;
         pl.b = 32;
         pl.C = (n_max + pl.P * pl.b - 1) / (pl.P * pl.b);
@@ -373,7 +383,7 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
         FP.tabs = fd.tabs;
         FusedKernel k;
         size_t smem;
-        fused_kernel(pl.B, pl.NR, &k, &smem);
+        fused_kernel(pl.B, pl.NR, pl.P, &k, &smem);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(pl.C, FP.Gc, nsub);
         cfg.blockDim = block;
@@ -489,7 +499,7 @@ kfp_status build_fused_tables(kfp_problem pb, const Plan &pl, std::vector<double
         c[(size_t)j * kc + 1] = (double)(qa * nu);
         for (int r = 0; r < pb->f_rank; ++r) c[(size_t)j * kc + 2 + r] = (double)(qa * (*fv_host)[(size_t)r * nn + j]);
     }
-    const int kQ = ((kfp::kFusedWarps * pl.B + 2) + 1) / 2 * 2;
+    const int kQ = ((pl.P * pl.B + 2) + 1) / 2 * 2;
     std::vector<double> t(2 * kQ + 2 * pl.B, 0.0);
     const long double q = pb->q;
     long double qq = 1.0L, ss = 0.0L;
@@ -546,7 +556,7 @@ kfp_status configure_kernels(Plan &pl) {
     if (pl.fused) {
         FusedKernel k;
         size_t smem;
-        fused_kernel(pl.B, pl.NR, &k, &smem);
+        fused_kernel(pl.B, pl.NR, pl.P, &k, &smem);
         KFP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(pl.C, 1024, 1);

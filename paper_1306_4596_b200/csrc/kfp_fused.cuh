@@ -32,7 +32,7 @@ namespace kfp {
 // 16-B aligned global column (a box starting at an odd column faults)
 constexpr int kHalo = 2;
 constexpr int kTW = kWarp + 2 * kHalo;       // 36 doubles (288 B) per smem tile row
-constexpr int kFusedWarps = 16;              // P
+constexpr int kFusedWarpsMax = 16;           // largest P (warps per CTA) instantiated
 constexpr int kNRmax = 4;                    // forcing ranks supported by the coefficient table
 constexpr int kMaxFusedCluster = 8;          // portable cluster size
 constexpr int kL2N = 22;                     // inputs of the level-2 map: F_0..7, G_0..7, x~ at 4 rows, g_lo, g_hi
@@ -96,24 +96,24 @@ constexpr int slot_doubles() {
     return ((B * kTW * 8 + 127) / 128) * 128 / 8;
 }
 // q^k and s2(k) tables for k <= R + 1 (R <= P B), rounded to an even count (16-B bulk copies)
-template <int B>
+template <int B, int P>
 __host__ __device__ constexpr int fused_kq() {
-    return ((kFusedWarps * B + 2) + 1) / 2 * 2;
+    return ((P * B + 2) + 1) / 2 * 2;
 }
 
-template <int B, int NR>
+template <int B, int NR, int P>
 struct FusedSmem {
     static constexpr int kSlot = slot_doubles<B>();
-    static constexpr int kRows = kFusedWarps * B;
+    static constexpr int kRows = P * B;
     static constexpr int kCoef = 2 + NR;  // c0', c1', g_0' .. g_{NR-1}'
-    static constexpr int kQ = fused_kq<B>();
+    static constexpr int kQ = fused_kq<B, P>();
     static constexpr int kTab = 2 * kQ + 2 * B;
-    alignas(128) double tile[kFusedWarps * kSlot];  // per warp: u^n rows [L][36]
+    alignas(128) double tile[P * kSlot];  // per warp: u^n rows [L][36]
     alignas(16) double coef[kRows * kCoef];         // per warp: its chunk's rows of coefT
     alignas(16) double tab[kTab];                   // qp[kQ] | s2[kQ] | kr[2B]  (copy of FusedParams::tabs)
     alignas(16) double l2m[kL2M];                   // level-2 map of this (subdomain, block)
-    double he[kFusedWarps * kCS];          // y at the chunk's last row (zero carry); then final Y carries
-    double ks[kFusedWarps * kCS];          // k at the chunk's first row (zero carry); then final X carries
+    double he[P * kCS];          // y at the chunk's last row (zero carry); then final Y carries
+    double ks[P * kCS];          // k at the chunk's first row (zero carry); then final X carries
     double kb[4 * kCS];                    // k at the column's rows 0,1,n-2,n-1 (chunk-local zero carries)
     double2 rFG[2][kMaxFusedCluster * kCS];  // received (F, G) per block, double-buffered by tile parity
     double rA[2][4 * kCS];                 // received x~ at rows 0,1,n-2,n-1 (zero column carries)
@@ -121,15 +121,15 @@ struct FusedSmem {
     double rtr[2][2 * kWarp];              // raw r at the outgoing-trace rows (by tile parity)
     double xsp[6 * kWarp];                 // x at the special rows: trace rows (c, c+1 | c, c-1), rows 0, n-1
     SubDev sd;                             // this subdomain's descriptor
-    double red[2 * kFusedWarps];
-    uint64_t bar[kFusedWarps];             // per warp: u^n tile (+ coefficient rows on the first tile)
+    double red[2 * P];
+    uint64_t bar[P];             // per warp: u^n tile (+ coefficient rows on the first tile)
     uint64_t tbar;                         // tables
     uint64_t xbar[2];                      // cluster exchange, by tile parity
 };
 
-template <int B, int NR>
+template <int B, int NR, int P>
 __host__ __device__ constexpr size_t fused_smem_bytes() {
-    return sizeof(FusedSmem<B, NR>);
+    return sizeof(FusedSmem<B, NR, P>);
 }
 
 // --------------------------------------------------------------------------- passes
@@ -215,9 +215,11 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 
 // --------------------------------------------------------------------------- the kernel
-template <int B, int NR>
-__global__ void __launch_bounds__(kFusedWarps * kWarp, 1) step_fused_tma(const FusedParams FP) {
-    using Sm = FusedSmem<B, NR>;
+template <int B, int NR, int P_>
+__global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const FusedParams FP) {
+    constexpr int NW = P_;            // warps (= chunks) per CTA
+    constexpr int kCPW = kWarp / NW;  // columns per warp in the transposed phase
+    using Sm = FusedSmem<B, NR, NW>;
     extern __shared__ __align__(128) char smraw[];
     Sm &sm = *reinterpret_cast<Sm *>(smraw);
     const StepParams &P = FP.S;
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 1) step_fused_tma(const F
         __syncthreads();
     }
     const SubDev &S = sm.sd;
-    const int n = S.n, L = FP.L, R = kFusedWarps * L;
+    const int n = S.n, L = FP.L, R = NW * L;
     const int rb0 = blk * R;                                    // first unknown row of this block
     const int Rb = max(0, min(R, n - rb0));                     // rows of this block
     const int s_w = warp * L;                                   // chunk start (block-local)
@@ -391,10 +393,10 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 1) step_fused_tma(const F
         KFP_T(2)
         __syncthreads();
 
-        // ---- levels 1 and 2 in the transposed layout: warp w, half lane>>4 owns column
-        //      col = 2w + (lane>>4); lane k = lane & 15 stands for chunk k of the block.
+        // ---- levels 1 and 2 in the transposed layout: warp w owns the kCPW columns
+        //      col = kCPW w + lane / NW; lane k = lane % NW stands for chunk k of the block.
         {
-            const int col = 2 * warp + (lane >> 4), k = lane & 15;
+            const int col = kCPW * warp + lane / NW, k = lane % NW;
             const int sk = k * L, Lk = max(0, min(L, Rb - sk)), ek = sk + Lk;
             const double Qk = qp[Lk];
             // level 1: affine Kogge-Stone scans over the chunks (zero block carries)
@@ -402,30 +404,30 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 1) step_fused_tma(const F
             double A = Qk, Bv = sm.he[k * kCS + col];
             const double ksk = sm.ks[k * kCS + col];
 #pragma unroll
-            for (int d = 1; d < 16; d <<= 1) {
-                const double Au = __shfl_up_sync(0xffffffffu, A, d, 16), Bu = __shfl_up_sync(0xffffffffu, Bv, d, 16);
+            for (int d = 1; d < NW; d <<= 1) {
+                const double Au = __shfl_up_sync(0xffffffffu, A, d, NW), Bu = __shfl_up_sync(0xffffffffu, Bv, d, NW);
                 if (k >= d) {
                     Bv = fma(A, Bu, Bv);
                     A *= Au;
                 }
             }
-            const double F = __shfl_sync(0xffffffffu, Bv, 15, 16);  // y at the block's last row
-            double y0 = __shfl_up_sync(0xffffffffu, Bv, 1, 16);
+            const double F = __shfl_sync(0xffffffffu, Bv, NW - 1, NW);  // y at the block's last row
+            double y0 = __shfl_up_sync(0xffffffffu, Bv, 1, NW);
             if (k == 0) y0 = 0.0;
             const double z0 = (Lk > 0) ? fma(kap_s(qp, s2, 0, Lk), y0, ksk) : 0.0;
             A = Qk;
             Bv = z0;
 #pragma unroll
-            for (int d = 1; d < 16; d <<= 1) {
-                const double Ad = __shfl_down_sync(0xffffffffu, A, d, 16), Bd = __shfl_down_sync(0xffffffffu, Bv, d, 16);
-                if (k + d < 16) {
+            for (int d = 1; d < NW; d <<= 1) {
+                const double Ad = __shfl_down_sync(0xffffffffu, A, d, NW), Bd = __shfl_down_sync(0xffffffffu, Bv, d, NW);
+                if (k + d < NW) {
                     Bv = fma(A, Bd, Bv);
                     A *= Ad;
                 }
             }
-            const double G = __shfl_sync(0xffffffffu, Bv, 0, 16);   // x at the block's first row
-            double x0 = __shfl_down_sync(0xffffffffu, Bv, 1, 16);
-            if (k == 15) x0 = 0.0;
+            const double G = __shfl_sync(0xffffffffu, Bv, 0, NW);   // x at the block's first row
+            double x0 = __shfl_down_sync(0xffffffffu, Bv, 1, NW);
+            if (k == NW - 1) x0 = 0.0;
             // push this block's aggregates of column col into every block of the cluster
             if (k == 0)
                 for (int c = 0; c < nblk; ++c) st_async_v2(&sm.rFG[par][blk * kCS + col], c, F, G, &sm.xbar[par]);
@@ -444,25 +446,30 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 1) step_fused_tma(const F
             KFP_T(3)
             mbar_wait(&sm.xbar[par], (it >> 1) & 1);
             KFP_T(4)
-            // level 2: block carries = the precomputed linear map of (F_c, G_c, x~_q, g_lo, g_hi),
-            // terms j = k and j = k + 16 on lane k, summed over the 16 lanes of the column
+            // level 2: block carries = the precomputed linear map of (F_c, G_c, x~_q, g_lo, g_hi);
+            // terms j = k, k + P, ... on lane k, summed over the NW lanes of the column
             double yv = 0.0, xv = 0.0;
-            {
-                const int c = k & 7;  // j = k: F_k (k < 8) or G_{k-8}
-                double v = 0.0;
-                if (c < nblk) v = (k < 8) ? sm.rFG[par][c * kCS + col].x : sm.rFG[par][c * kCS + col].y;
-                yv = sm.l2m[k] * v;
-                xv = sm.l2m[24 + k] * v;
-            }
-            if (k < kL2N - 16) {  // j = 16 + k: x~_0..3, g_lo, g_hi
-                const double v = (k < 4) ? sm.rA[par][k * kCS + col] : sm.gin[(k - 4) * kWarp + col];
-                yv = fma(sm.l2m[16 + k], v, yv);
-                xv = fma(sm.l2m[24 + 16 + k], v, xv);
+#pragma unroll
+            for (int j0 = 0; j0 < kL2N; j0 += NW) {
+                const int j = j0 + k;
+                if (j < kL2N) {
+                    double v = 0.0;
+                    if (j < 16) {
+                        const int c = j & 7;
+                        if (c < nblk) v = (j < 8) ? sm.rFG[par][c * kCS + col].x : sm.rFG[par][c * kCS + col].y;
+                    } else if (j < 20) {
+                        v = sm.rA[par][(j - 16) * kCS + col];
+                    } else {
+                        v = sm.gin[(j - 20) * kWarp + col];
+                    }
+                    yv = fma(sm.l2m[j], v, yv);
+                    xv = fma(sm.l2m[24 + j], v, xv);
+                }
             }
 #pragma unroll
-            for (int o = 8; o > 0; o >>= 1) {
-                yv += __shfl_xor_sync(0xffffffffu, yv, o, 16);
-                xv += __shfl_xor_sync(0xffffffffu, xv, o, 16);
+            for (int o = NW / 2; o > 0; o >>= 1) {
+                yv += __shfl_xor_sync(0xffffffffu, yv, o, NW);
+                xv += __shfl_xor_sync(0xffffffffu, xv, o, NW);
             }
             // final carries of chunk k: y just above it, x just below it
             sm.he[k * kCS + col] = fma(qp[sk], yv, y0);
@@ -570,14 +577,14 @@ __global__ void __launch_bounds__(kFusedWarps * kWarp, 1) step_fused_tma(const F
         et = warp_max(et);
         if (lane == 0) {
             sm.red[warp] = eif;
-            sm.red[kFusedWarps + warp] = et;
+            sm.red[NW + warp] = et;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             double a = 0.0, b = 0.0;
-            for (int c = 0; c < kFusedWarps; ++c) {
+            for (int c = 0; c < NW; ++c) {
                 a = fmax(a, sm.red[c]);
-                b = fmax(b, sm.red[kFusedWarps + c]);
+                b = fmax(b, sm.red[NW + c]);
             }
             if (a > 0.0) atomic_max_pos(P.errIF, a);
             if (b > 0.0 && P.errT) atomic_max_pos(P.errT, b);
