@@ -22,6 +22,7 @@
 #include "../../include/kfp.h"
 #include "kfp_device.cuh"
 #include "kfp_fused.cuh"
+#include "kfp_window.cuh"
 
 using kfp::SubDev;
 using kfp::StepParams;
@@ -49,6 +50,7 @@ void set_err(const char *fmt, ...) {
     } while (0)
 
 struct Plan {
+    bool window = false; // persistent pipelined window kernel (one launch per SWR iteration); implies fused geometry
     bool fused = false;  // fused TMA/cluster kernel; else the three-phase path
     int P = 8, b = 32, R = 256, C = 1;
     int L = 0, B = 0, NR = 2;  // fused: chunk rows, register-array size (template), forcing ranks (template)
@@ -60,6 +62,10 @@ struct Plan {
 struct FusedData {
     CUtensorMap *maps = nullptr;  // [2][nsub][2]: load maps then store maps
     double *l2c = nullptr, *coefT = nullptr, *tabs = nullptr;
+    // window kernel
+    double *cfn = nullptr;               // [nt][kMaxRank] dt ft_r(t_{n+1})
+    unsigned int *flags = nullptr;       // [nsub][ntiles][C] step flags
+    unsigned int *fault = nullptr;       // watchdog word
 };
 
 using FusedKernel = void (*)(const kfp::FusedParams);
@@ -83,14 +89,73 @@ bool fused_kernel(int B, int NR, int P, FusedKernel *k, size_t *smem) {
 }
 constexpr int kBs[] = {8, 16, 17, 32, 33};
 
+using WindowKernel = void (*)(const kfp::WinParams);
+template <int B, int NR, int P>
+void window_entry(WindowKernel *k, size_t *smem) {
+    *k = kfp::step_window<B, NR, P>;
+    *smem = kfp::window_smem_bytes<B, NR, P>();
+}
+// instantiated (B, NR, P) combinations of the window kernel (P = 16 warps, 1 CTA per SM)
+bool window_kernel(int B, int NR, int P, WindowKernel *k, size_t *smem) {
+#define KFP_WENTRY(BB, NN, PP)             \
+    if (B == BB && NR == NN && P == PP) {  \
+        window_entry<BB, NN, PP>(k, smem); \
+        return true;                       \
+    }
+    KFP_WENTRY(8, 2, 8) KFP_WENTRY(16, 2, 8) KFP_WENTRY(17, 2, 8) KFP_WENTRY(32, 2, 8) KFP_WENTRY(33, 2, 8)
+    KFP_WENTRY(8, 4, 8) KFP_WENTRY(16, 4, 8) KFP_WENTRY(17, 4, 8) KFP_WENTRY(32, 4, 8) KFP_WENTRY(33, 4, 8)
+#undef KFP_WENTRY
+    return false;
+}
+constexpr int kWBs[] = {8, 16, 17, 32, 33};
+
 // Launch geometry for columns of at most n_max unknown rows.
 // Fused path: P = 16 warps per CTA, chunks of L rows (target 17), row blocks of
 // R = 16 L rows, C = ceil(n_max / R) <= 8 CTAs per cluster.  Otherwise the
 // three-phase path (P = 8, b = 32, block aggregates through global memory).
-Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused) {
+Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool allow_window = false) {
     Plan pl;
     const int n_max = *std::max_element(ns.begin(), ns.end());
     const int NR = (f_rank <= 2) ? 2 : 4;
+    // Window kernel (SWR iterations): P = 8 warps (1 CTA per SM, 255 registers: two tiles' rows in
+    // registers), chunks of L <= 33 rows, C <= 8 CTAs per cluster.
+    // Opt-in (KFP_WINDOW=1): correct, but measured slower than the per-step kernel on c2.
+    if (allow_window && allow_fused && getenv("KFP_WINDOW") && !getenv("KFP_NO_WINDOW") && f_rank <= kfp::kNRmax) {
+        const int P = 8;
+        int C = 1;
+        while (C < 8 && (n_max + P * C - 1) / (P * C) > 33) ++C;
+        int L = (n_max + P * C - 1) / (P * C);
+        for (bool ok = false; !ok && L <= 33;) {
+            ok = true;
+            for (int n : ns)
+                if (n % (P * L) == 1) ok = false;
+            if (!ok) ++L;
+        }
+        int B = 0;
+        for (int bb : kWBs)
+            if (bb >= L) {
+                B = bb;
+                break;
+            }
+        WindowKernel k;
+        size_t smem = 0;
+        if (B > 0 && L <= 33 && window_kernel(B, NR, P, &k, &smem)) {
+            pl.window = pl.fused = true;
+            pl.P = P;
+            pl.C = C;
+            pl.L = L;
+            pl.B = B;
+            pl.NR = NR;
+            pl.b = L;
+            pl.R = P * L;
+            pl.smem = smem;
+            char buf[200];
+            snprintf(buf, sizeof buf, "window-pipelined P=%d L=%d (B=%d) R=%d C=%d NR=%d smem=%zu", P, L, B, pl.R, C, NR,
+                     smem);
+            pl.text = buf;
+            return pl;
+        }
+    }
     // P = 8 warps (2 CTAs per SM) first, then P = 16 (1 CTA per SM): the smallest cluster whose
     // warps hold at most 33 rows; the column's first/last row blocks must hold >= 2 rows.
     const char *force = getenv("KFP_FORCE_P");  // debugging / experiments only
@@ -209,6 +274,7 @@ struct kfp_problem_s {
     double *edge_sendR[2] = {nullptr, nullptr}, *edge_recvR[2] = {nullptr, nullptr};
     std::vector<double *> zero_on_reset;  // parity-0 incoming buffers
 
+    unsigned int epoch = 0;  // window kernel: base of the step-flag values of the next launch
     int64_t launches = 0;
     std::vector<cudaEvent_t> ev;  // 2 per iteration of the last iterate call + 2 around it
     int ev_used = 0;
@@ -369,6 +435,10 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
     P.C = pl.C;
     const int ntiles = (pb->nx + kfp::kWarp - 1) / kfp::kWarp;
     const dim3 block(pl.P * kfp::kWarp);
+    if (pl.window) {
+        set_err("launch_step: the window plan has no per-step kernel");
+        return KFP_E_STATE;
+    }
     if (pl.fused) {
         kfp::FusedParams FP;
         FP.S = P;
@@ -407,6 +477,80 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
         pb->launches += 3;
     }
     KFP_CUDA(cudaGetLastError());
+    return KFP_OK;
+}
+
+// One persistent launch of the window kernel: steps [n0, n1) of every local subdomain.
+kfp_status launch_window(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, const FusedData &fd, int n0, int n1) {
+    P.P = pl.P;
+    P.b = pl.b;
+    P.R = pl.R;
+    P.C = pl.C;
+    const int ntiles = (pb->nx + kfp::kWarp - 1) / kfp::kWarp;
+    kfp::WinParams W;
+    W.S = P;
+    W.tmaps = fd.maps;
+    W.l2m = fd.l2c;
+    W.coefT = fd.coefT;
+    W.tabs = fd.tabs;
+    W.cfn = fd.cfn;
+    W.flags = fd.flags;
+    W.fault = fd.fault;
+    W.L = pl.L;
+    W.ntiles = ntiles;
+    W.nsub = nsub;
+    W.n0 = n0;
+    W.n1 = n1;
+    int G = std::min(pl.Gc_total, nsub * ntiles);
+    if (const char *e = getenv("KFP_WIN_G")) G = std::max(1, std::min(G, atoi(e)));  // experiments only (<= resident)
+    W.G = G;
+    W.epoch = pb->epoch;
+    W.dbg = getenv("KFP_WIN_DBG") ? atoi(getenv("KFP_WIN_DBG")) : 0;  // experiments only
+    pb->epoch += (unsigned int)pb->nt + 1u;
+    WindowKernel k;
+    size_t smem;
+    window_kernel(pl.B, pl.NR, pl.P, &k, &smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.C, G, 1);
+    cfg.blockDim = dim3(pl.P * kfp::kWarp);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = pb->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = pl.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    KFP_CUDA(cudaLaunchKernelEx(&cfg, k, W));
+    pb->launches += 1;
+    KFP_CUDA(cudaGetLastError());
+    return KFP_OK;
+}
+
+// Window-kernel tables: dt ft_r(t_{n+1}) per step, zeroed step flags, watchdog word.
+kfp_status build_window_tables(kfp_problem pb, const Plan &pl, int nsub, FusedData *fd, std::vector<void *> *owner) {
+    if (!pl.window) return KFP_OK;
+    const int nt = pb->nt, ntiles = (pb->nx + kfp::kWarp - 1) / kfp::kWarp;
+    std::vector<double> cfn((size_t)nt * kfp::kMaxRank, 0.0);
+    for (int n = 0; n < nt; ++n)
+        for (int r = 0; r < pb->f_rank; ++r)  // the same product launch_step forms on the host
+            cfn[(size_t)n * kfp::kMaxRank + r] = pb->dt * pb->ft[(size_t)r * (nt + 1) + n + 1];
+    void *d1 = nullptr, *d2 = nullptr, *d3 = nullptr;
+    const size_t nflags = (size_t)nsub * ntiles * pl.C;
+    KFP_CUDA(cudaMalloc(&d1, sizeof(double) * cfn.size()));
+    owner->push_back(d1);
+    KFP_CUDA(cudaMemcpy(d1, cfn.data(), sizeof(double) * cfn.size(), cudaMemcpyHostToDevice));
+    KFP_CUDA(cudaMalloc(&d2, sizeof(unsigned int) * nflags));
+    owner->push_back(d2);
+    KFP_CUDA(cudaMemset(d2, 0, sizeof(unsigned int) * nflags));
+    KFP_CUDA(cudaMalloc(&d3, 16));
+    owner->push_back(d3);
+    KFP_CUDA(cudaMemset(d3, 0, 16));
+    fd->cfn = static_cast<double *>(d1);
+    fd->flags = static_cast<unsigned int *>(d2);
+    fd->fault = static_cast<unsigned int *>(d3);
+    pb->epoch = 0;
     return KFP_OK;
 }
 
@@ -553,7 +697,30 @@ kfp_status build_tmaps(kfp_problem pb, const Plan &pl, const std::vector<SubDev>
 }
 
 kfp_status configure_kernels(Plan &pl) {
-    if (pl.fused) {
+    if (pl.window) {
+        WindowKernel k;
+        size_t smem;
+        window_kernel(pl.B, pl.NR, pl.P, &k, &smem);
+        KFP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(pl.C, 1024, 1);
+        cfg.blockDim = dim3(pl.P * kfp::kWarp);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = pl.C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        KFP_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
+        if (ncl < 1) {
+            set_err("window kernel: no cluster of %d CTAs (%zu B smem) fits on the device", pl.C, smem);
+            return KFP_E_CUDA;
+        }
+        pl.Gc_total = ncl;
+    } else if (pl.fused) {
         FusedKernel k;
         size_t smem;
         fused_kernel(pl.B, pl.NR, pl.P, &k, &smem);
@@ -920,7 +1087,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
     }
     std::vector<int> ns;
     for (const SubDev &sd : pb->subs) ns.push_back(sd.n);
-    pb->plan = make_plan(ns, pb->f_rank, true);
+    pb->plan = make_plan(ns, pb->f_rank, true, true);
     Plan &pl = pb->plan;
     // the rows of each outgoing trace stencil must sit in one row block
     for (int i = 0; i < nloc; ++i) {
@@ -1002,6 +1169,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
         kfp_status st = build_tmaps(pb, pl, pb->subs, &pb->fd.maps, &own);
         if (!st) st = build_l2m(pb, pl, pb->subs, &pb->fd.l2c, &own);
         if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &pb->fd.coefT, &pb->fd.tabs, &own);
+        if (!st) st = build_window_tables(pb, pl, nloc, &pb->fd, &own);
         for (void *q : own) pb->swr_allocs.push_back(static_cast<double *>(q));
         if (st) return st;
     }
@@ -1064,9 +1232,13 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
         P.errT = pb->d_errT + (k - 1);
         P.errIF = pb->d_errIF + (k - 1);
         KFP_CUDA(cudaEventRecord(pb->ev[2 + 2 * it], pb->stream));
-        for (int n = 0; n < pb->nt; ++n) {
-            P.last = (n + 1 == pb->nt);
-            if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n, pb->fd)) return st;
+        if (pb->plan.window) {
+            if (kfp_status st = launch_window(pb, pb->plan, P, nloc, pb->fd, 0, pb->nt)) return st;
+        } else {
+            for (int n = 0; n < pb->nt; ++n) {
+                P.last = (n + 1 == pb->nt);
+                if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n, pb->fd)) return st;
+            }
         }
         KFP_CUDA(cudaEventRecord(pb->ev[3 + 2 * it], pb->stream));
         pb->k_done = k;
@@ -1209,11 +1381,26 @@ kfp_status kfp_swr_trace(kfp_problem pb, int32_t i, int32_t dir, double *out) {
 int64_t kfp_launch_count(kfp_problem pb) { return pb ? pb->launches : -1; }
 
 #ifdef KFP_TRACE
+// debug builds only: one traced SWR iteration (window plans) -> per-CTA accumulated phase times [cta][64]
+extern "C" int kfp_debug_trace_window(kfp_problem pb, unsigned long long *host, int cap) {
+    unsigned long long *d = nullptr;
+    cudaMalloc(&d, sizeof(unsigned long long) * cap * 64);
+    cudaMemset(d, 0, sizeof(unsigned long long) * cap * 64);
+    cudaMemcpyToSymbol(kfp::g_kfp_trace, &d, sizeof(d));
+    kfp_swr_reset(pb);
+    kfp_swr_iterate(pb, 1);
+    cudaDeviceSynchronize();
+    unsigned long long *z = nullptr;
+    cudaMemcpyToSymbol(kfp::g_kfp_trace, &z, sizeof(z));
+    cudaMemcpy(host, d, sizeof(unsigned long long) * cap * 64, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return (int)cudaGetLastError();
+}
 // debug builds only (not part of include/kfp.h): one traced step launch of the current setup
 extern "C" int kfp_debug_trace_step(kfp_problem pb, int n, unsigned long long *host, int cap) {
     unsigned long long *d = nullptr;
-    cudaMalloc(&d, sizeof(unsigned long long) * cap * 8);
-    cudaMemset(d, 0, sizeof(unsigned long long) * cap * 8);
+    cudaMalloc(&d, sizeof(unsigned long long) * cap * 64);
+    cudaMemset(d, 0, sizeof(unsigned long long) * cap * 64);
     cudaMemcpyToSymbol(kfp::g_kfp_trace, &d, sizeof(d));
     StepParams P = base_params(pb);
     P.subs = pb->d_subs;
@@ -1230,7 +1417,7 @@ extern "C" int kfp_debug_trace_step(kfp_problem pb, int n, unsigned long long *h
     cudaDeviceSynchronize();
     unsigned long long *z = nullptr;
     cudaMemcpyToSymbol(kfp::g_kfp_trace, &z, sizeof(z));
-    cudaMemcpy(host, d, sizeof(unsigned long long) * cap * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(host, d, sizeof(unsigned long long) * cap * 64, cudaMemcpyDeviceToHost);
     cudaFree(d);
     return (int)cudaGetLastError();
 }

@@ -105,13 +105,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+// The waiting thread may be suspended (up to the hint, 1 ms) instead of spinning, so that a
+// co-resident CTA gets the issue slots; it resumes when the phase completes.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n .reg .pred p;\n"
         "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 // Bulk asynchronous copy global -> shared (TMA engine, no tensor map);
@@ -128,6 +130,10 @@ __device__ __forceinline__ void cluster_arrive() {
 }
 __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// st.global through a generic pointer known to address global memory (the slabs)
+__device__ __forceinline__ void st_global_f64(double *p, double v) {
+    asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v));
 }
 __device__ __forceinline__ void st_cs(double *p, double v) {  // streaming store (evict-first)
     asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");

@@ -208,10 +208,17 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define KFP_T(k)                                                                                            \
     if (g_kfp_trace && threadIdx.x == 0) {                                                                  \
         const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; \
-        g_kfp_trace[cta * 8 + (k)] = gtime();                                                               \
+        g_kfp_trace[cta * 64 + (k)] = gtime();                                                              \
+    }
+// per-tile event e (0..5) of tile iteration `it` (first 9 tiles)
+#define KFP_TT(e)                                                                                           \
+    if (g_kfp_trace && threadIdx.x == 0 && it < 9) {                                                        \
+        const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; \
+        g_kfp_trace[cta * 64 + 2 + 6 * it + (e)] = gtime();                                                 \
     }
 #else
 #define KFP_T(k)
+#define KFP_TT(e)
 #endif
 
 // --------------------------------------------------------------------------- the kernel
@@ -319,6 +326,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
         double hend = 0.0, kst = 0.0;
         if (Lw > 0) {
             if (!P.from_u0 || it == 0) mbar_wait(&sm.bar[warp], par);
+            KFP_TT(0)
             if (P.from_u0) {  // u^0 from the separable u0 tables (0 B of HBM), incl. the halo columns
                 for (int l = 0; l < Lw; ++l) {
                     const int j = S.first + cr0 + l;
@@ -390,7 +398,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
         sm.he[warp * kCS + lane] = hend;
         sm.ks[warp * kCS + lane] = kst;
         if (it == 0) mbar_wait(&sm.tbar, 0);  // tables (long since arrived)
-        KFP_T(2)
+        KFP_TT(1)
         __syncthreads();
 
         // ---- levels 1 and 2 in the transposed layout: warp w owns the kCPW columns
@@ -443,9 +451,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             if (threadIdx.x == 0)
                 mbar_expect_tx(&sm.xbar[par],
                                static_cast<uint32_t>(nblk * kWarp * sizeof(double2) + 4 * kWarp * sizeof(double)));
-            KFP_T(3)
+            KFP_TT(2)
             mbar_wait(&sm.xbar[par], (it >> 1) & 1);
-            KFP_T(4)
+            KFP_TT(3)
             // level 2: block carries = the precomputed linear map of (F_c, G_c, x~_q, g_lo, g_hi);
             // terms j = k, k + P, ... on lane k, summed over the NW lanes of the column
             double yv = 0.0, xv = 0.0;
@@ -475,7 +483,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             sm.he[k * kCS + col] = fma(qp[sk], yv, y0);
             sm.ks[k * kCS + col] = fma(qp[Rb - ek], xv, fma(kap_s(qp, s2, ek, Rb), yv, x0));
         }
-        KFP_T(5)
+        KFP_TT(4)
         __syncthreads();
 
         // ---- pass C: x = k + kap Y + rho X; coalesced stores of u^{n+1}
@@ -492,9 +500,18 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                     if (l < Lw) h[l] = fma(kap_s(qp, s2, l, Lw), Y, fma(qp[Lw - l], X, h[l]));
             }
             if (active) {
+                if (Lw == B) {  // full chunk: unpredicated global stores, one pointer step per row
+                    double *p = dst;
 #pragma unroll
-                for (int l = 0; l < B; ++l)
-                    if (l < Lw) dst[l * pitch] = h[l];
+                    for (int l = 0; l < B; ++l) {
+                        st_global_f64(p, h[l]);
+                        p += pitch;
+                    }
+                } else {
+#pragma unroll
+                    for (int l = 0; l < B; ++l)
+                        if (l < Lw) dst[l * pitch] = h[l];
+                }
             }
             if (P.last && active) {  // error at T on every unknown row (a 1/N_t fraction of the steps)
                 const double *ut = P.UT + static_cast<size_t>(S.first + cr0) * P.nx + m;
@@ -567,7 +584,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                     }
             }
         }
-        KFP_T(6)
+        KFP_TT(5)
     }
     grid_dep_launch();  // the next step may start its prologue
 
@@ -590,7 +607,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             if (b > 0.0 && P.errT) atomic_max_pos(P.errT, b);
         }
     }
-    KFP_T(7)
+    KFP_T(63)
 }
 
 }  // namespace kfp
