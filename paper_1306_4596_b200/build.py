@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "kfp_api.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "kfp_fused.cuh"), os.path.join(HERE, "csrc", "kfp_window.cuh"), os.path.join(HERE, "csrc", "kfp_device.cuh"), os.path.join(ROOT, "include", "kfp.h")]
+DEPS = SRC + [os.path.join(HERE, "csrc", "kfp_fused.cuh"), os.path.join(HERE, "csrc", "kfp_window.cuh"), os.path.join(HERE, "csrc", "kfp_col.cuh"), os.path.join(HERE, "csrc", "kfp_device.cuh"), os.path.join(ROOT, "include", "kfp.h")]
 LIB = os.path.join(HERE, "libkfp.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

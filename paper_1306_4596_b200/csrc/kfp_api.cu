@@ -23,6 +23,7 @@
 #include "kfp_device.cuh"
 #include "kfp_fused.cuh"
 #include "kfp_window.cuh"
+#include "kfp_col.cuh"
 
 using kfp::SubDev;
 using kfp::StepParams;
@@ -50,11 +51,13 @@ void set_err(const char *fmt, ...) {
     } while (0)
 
 struct Plan {
+    bool col = false;    // cluster-free column-tile kernel (kfp_col.cuh): 8 columns x the whole column per CTA
     bool window = false; // persistent pipelined window kernel (one launch per SWR iteration); implies fused geometry
     bool fused = false;  // fused TMA/cluster kernel; else the three-phase path
     int P = 8, b = 32, R = 256, C = 1;
     int L = 0, B = 0, NR = 2;  // fused: chunk rows, register-array size (template), forcing ranks (template)
     int Gc_total = 1;          // fused: co-resident clusters (persistent grid size over all subdomains)
+                               // col: co-resident CTAs
     size_t smem = 0;
     std::string text;
 };
@@ -66,6 +69,10 @@ struct FusedData {
     double *cfn = nullptr;               // [nt][kMaxRank] dt ft_r(t_{n+1})
     unsigned int *flags = nullptr;       // [nsub][ntiles][C] step flags
     unsigned int *fault = nullptr;       // watchdog word
+    // column-tile kernel
+    double *ctab = nullptr;              // [nsub][NC][kCT] chunk constants
+    double *ctabs = nullptr;             // qp | s2 | kr of the column kernel
+    double *fvq = nullptr;               // [nv+1][NR] (q/a) fv_r(j)
 };
 
 using FusedKernel = void (*)(const kfp::FusedParams);
@@ -109,14 +116,65 @@ bool window_kernel(int B, int NR, int P, WindowKernel *k, size_t *smem) {
 }
 constexpr int kWBs[] = {8, 16, 17, 32, 33};
 
+using ColKernel = void (*)(const kfp::ColParams);
+template <int B, int NR, int P>
+void col_entry(ColKernel *k, size_t *smem) {
+    *k = kfp::step_col<B, NR, P>;
+    *smem = kfp::col_smem_bytes<B, NR, P>();
+}
+// instantiated (B, NR, P) combinations of the column-tile kernel
+bool col_kernel(int B, int NR, int P, ColKernel *k, size_t *smem) {
+#define KFP_CENTRY(BB, NN, PP)          \
+    if (B == BB && NR == NN && P == PP) { \
+        col_entry<BB, NN, PP>(k, smem);   \
+        return true;                      \
+    }
+    KFP_CENTRY(8, 2, 8) KFP_CENTRY(16, 2, 8) KFP_CENTRY(17, 2, 8) KFP_CENTRY(32, 2, 8) KFP_CENTRY(33, 2, 8)
+    KFP_CENTRY(8, 2, 16) KFP_CENTRY(16, 2, 16) KFP_CENTRY(17, 2, 16) KFP_CENTRY(32, 2, 16) KFP_CENTRY(33, 2, 16)
+#undef KFP_CENTRY
+    return false;
+}
+
 // Launch geometry for columns of at most n_max unknown rows.
 // Fused path: P = 16 warps per CTA, chunks of L rows (target 17), row blocks of
 // R = 16 L rows, C = ceil(n_max / R) <= 8 CTAs per cluster.  Otherwise the
 // three-phase path (P = 8, b = 32, block aggregates through global memory).
-Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool allow_window = false) {
+Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool allow_window = false, int nx = 0) {
     Plan pl;
     const int n_max = *std::max_element(ns.begin(), ns.end());
     const int NR = (f_rank <= 2) ? 2 : 4;
+    // Column-tile kernel (opt-in, KFP_COL=1; correct, but measured slower than the cluster kernel on c2
+    // and c4): 8-column tiles, the whole column in one CTA of P = 8 (2 CTAs per SM,
+    // n <= 1056) or 16 warps (n <= 2112), chunks of L <= 33 rows.
+    if (allow_fused && nx > 0 && nx % kfp::kColW == 0 && NR == 2 && getenv("KFP_COL") && !getenv("KFP_WINDOW") &&
+        n_max <= 4 * 16 * 33 && (int)ns.size() <= kfp::kColMaxSub) {
+        const int P = (n_max <= 4 * 8 * 33) ? 8 : 16;
+        int L = (n_max + 4 * P - 1) / (4 * P);
+        if (L % 2 == 0 && L < 33) ++L;  // odd: the 4 chunks of a warp alternate smem bank halves (64-B rows)
+        int B = 0;
+        for (int bb : kBs)
+            if (bb >= L) {
+                B = bb;
+                break;
+            }
+        ColKernel k;
+        size_t smem = 0;
+        if (B > 0 && col_kernel(B, NR, P, &k, &smem)) {
+            pl.col = pl.fused = true;
+            pl.P = P;
+            pl.C = 1;
+            pl.L = L;
+            pl.B = B;
+            pl.NR = NR;
+            pl.b = L;
+            pl.R = 4 * P * L;
+            pl.smem = smem;
+            char buf[200];
+            snprintf(buf, sizeof buf, "column-tile P=%d L=%d (B=%d) NC=%d W=8 NR=%d smem=%zu", P, L, B, 4 * P, NR, smem);
+            pl.text = buf;
+            return pl;
+        }
+    }
     // Window kernel (SWR iterations): P = 8 warps (1 CTA per SM, 255 registers: two tiles' rows in
     // registers), chunks of L <= 33 rows, C <= 8 CTAs per cluster.
     // Opt-in (KFP_WINDOW=1): correct, but measured slower than the per-step kernel on c2.
@@ -439,6 +497,37 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
         set_err("launch_step: the window plan has no per-step kernel");
         return KFP_E_STATE;
     }
+    if (pl.col) {
+        kfp::ColParams CP;
+        CP.S = P;
+        CP.tmaps = fd.maps;
+        CP.fvq = fd.fvq;
+        CP.ctab = fd.ctab;
+        CP.tabs = fd.ctabs;
+        CP.rec_rows = rec_rows;
+        CP.nrec = nrec;
+        CP.L = pl.L;
+        CP.ntiles = pb->nx / kfp::kColW;
+        CP.nsub = nsub;
+        CP.qdn = pb->q / pb->a * (pb->hv * pb->dt / pb->hx);
+        ColKernel k;
+        size_t smem;
+        col_kernel(pl.B, pl.NR, pl.P, &k, &smem);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(std::max(1, std::min(pl.Gc_total, nsub * CP.ntiles)));
+        cfg.blockDim = block;
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = pb->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        KFP_CUDA(cudaLaunchKernelEx(&cfg, k, CP));
+        pb->launches += 1;
+        KFP_CUDA(cudaGetLastError());
+        return KFP_OK;
+    }
     if (pl.fused) {
         kfp::FusedParams FP;
         FP.S = P;
@@ -554,6 +643,92 @@ kfp_status build_window_tables(kfp_problem pb, const Plan &pl, int nsub, FusedDa
     return KFP_OK;
 }
 
+// Column-tile kernel tables: tensor maps (box 8 x 4L), per-subdomain chunk constants
+// (q^{L_k}, kap(0, L_k), q^{s_k}, kap(e_k, n), q^{n-e_k}), qp | s2 | kr, and (q/a) fv_r(j).
+kfp_status build_col_tables(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, FusedData *fd,
+                            std::vector<void *> *owner) {
+    if (!pl.col) return KFP_OK;
+    const long double q = pb->q;
+    auto qpw = [&](long double e) { return powl(q, e); };
+    auto s2f = [&](int k) {  // sum_{t<k} q^{2t}
+        long double sacc = 0, t = 1;
+        for (int i = 0; i < k; ++i) {
+            sacc += t;
+            t *= q * q;
+        }
+        return sacc;
+    };
+    auto kap = [&](int r, int len) { return qpw(r + 1) * s2f(len - r); };
+    const size_t ns = subs.size();
+    const int NC = 4 * pl.P, L = pl.L;
+    // tensor maps
+    std::vector<CUtensorMap> maps(2 * ns);
+    for (size_t i = 0; i < ns; ++i)
+        for (int qq = 0; qq < 2; ++qq) {
+            double *base = subs[i].slab[qq] + (size_t)(subs[i].first - subs[i].lo) * pb->nx;
+            if (!make_tmap(&maps[2 * i + qq], base, pb->nx, subs[i].n, 2 * L, kfp::kColW)) {
+                set_err("cuTensorMapEncodeTiled failed (column tile, nx=%d rows=%d)", pb->nx, subs[i].n);
+                return KFP_E_CUDA;
+            }
+        }
+    // chunk constants
+    std::vector<double> ct(ns * NC * kfp::kCT, 0.0);
+    for (size_t i = 0; i < ns; ++i) {
+        const int n = subs[i].n;
+        for (int k = 0; k < NC; ++k) {
+            double *e = ct.data() + (i * NC + k) * kfp::kCT;
+            const int Lk = std::max(0, std::min(L, n - k * L)), sk = k * L, ek = sk + Lk;
+            if (Lk == 0) {
+                e[0] = 1.0;
+                continue;
+            }
+            e[0] = (double)qpw(Lk);
+            e[1] = (double)kap(0, Lk);
+            e[2] = (double)qpw(sk);
+            e[3] = (ek >= n) ? 0.0 : (double)kap(ek, n);
+            e[4] = (double)qpw(n - ek);
+        }
+    }
+    // qp | s2 | kr
+    const int kQ = ((pl.B + 2) + 1) / 2 * 2;
+    std::vector<double> t(2 * kQ + 2 * pl.B, 0.0);
+    {
+        long double qq = 1.0L, ss = 0.0L;
+        for (int k = 0; k < kQ; ++k) {
+            t[k] = (double)qq;
+            t[kQ + k] = (double)ss;
+            ss += qq * qq;
+            qq *= q;
+        }
+        for (int l = 0; l < L; ++l) {
+            t[2 * kQ + 2 * l] = (double)kap(l, L);
+            t[2 * kQ + 2 * l + 1] = (double)qpw(L - l);
+        }
+    }
+    // (q/a) fv_r(j), NR columns
+    const int nn = pb->nv + 1;
+    const long double qa = (long double)pb->q / pb->a;
+    std::vector<double> fv((size_t)nn * pl.NR, 0.0);
+    for (int j = 0; j < nn; ++j)
+        for (int r = 0; r < std::min(pb->f_rank, pl.NR); ++r) fv[(size_t)j * pl.NR + r] = (double)(qa * pb->fv_host[(size_t)r * nn + j]);
+    auto up = [&](const void *src, size_t bytes, void **dst) -> kfp_status {
+        KFP_CUDA(cudaMalloc(dst, bytes));
+        owner->push_back(*dst);
+        KFP_CUDA(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+        return KFP_OK;
+    };
+    void *d1 = nullptr, *d2 = nullptr, *d3 = nullptr, *d4 = nullptr;
+    if (kfp_status st = up(maps.data(), sizeof(CUtensorMap) * maps.size(), &d1)) return st;
+    if (kfp_status st = up(ct.data(), sizeof(double) * ct.size(), &d2)) return st;
+    if (kfp_status st = up(t.data(), sizeof(double) * t.size(), &d3)) return st;
+    if (kfp_status st = up(fv.data(), sizeof(double) * (fv.size() + 2), &d4)) return st;  // +2: 16-B bulk-copy tail
+    fd->maps = static_cast<CUtensorMap *>(d1);
+    fd->ctab = static_cast<double *>(d2);
+    fd->ctabs = static_cast<double *>(d3);
+    fd->fvq = static_cast<double *>(d4);
+    return KFP_OK;
+}
+
 // Level-2 linear maps (kfp_fused.cuh, kL2M layout): for every subdomain and row block
 // `me`, the block carries (Y_blk(me), X_blk(me)) as linear functions of the 22 inputs
 // v = (F_0..7, G_0..7, x~ at rows 0,1,n-2,n-1, g_lo, g_hi), obtained by running the
@@ -561,7 +736,7 @@ kfp_status build_window_tables(kfp_problem pb, const Plan &pl, int nsub, FusedDa
 kfp_status build_l2m(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, double **out,
                      std::vector<void *> *owner) {
     *out = nullptr;
-    if (!pl.fused) return KFP_OK;
+    if (!pl.fused || pl.col) return KFP_OK;
     const long double q = pb->q, a = pb->a;
     auto qp = [&](long double e) { return powl(q, e); };
     auto s2 = [&](int k) {  // sum_{t<k} q^{2t}
@@ -632,7 +807,7 @@ kfp_status build_l2m(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &
 kfp_status build_fused_tables(kfp_problem pb, const Plan &pl, std::vector<double> *fv_host, double **coefT,
                               double **tabs, std::vector<void *> *owner) {
     *coefT = *tabs = nullptr;
-    if (!pl.fused) return KFP_OK;
+    if (!pl.fused || pl.col) return KFP_OK;
     const int kc = 2 + pl.NR, nn = pb->nv + 1;
     const long double qa = (long double)pb->q / pb->a;
     std::vector<double> c((size_t)nn * kc, 0.0);
@@ -676,7 +851,7 @@ kfp_status build_fused_tables(kfp_problem pb, const Plan &pl, std::vector<double
 kfp_status build_tmaps(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, CUtensorMap **out,
                        std::vector<void *> *owner) {
     *out = nullptr;
-    if (!pl.fused) return KFP_OK;
+    if (!pl.fused || pl.col) return KFP_OK;
     const size_t ns = subs.size();
     std::vector<CUtensorMap> maps(4 * ns);
     for (size_t i = 0; i < ns; ++i)
@@ -697,6 +872,22 @@ kfp_status build_tmaps(kfp_problem pb, const Plan &pl, const std::vector<SubDev>
 }
 
 kfp_status configure_kernels(Plan &pl) {
+    if (pl.col) {
+        ColKernel k;
+        size_t smem;
+        col_kernel(pl.B, pl.NR, pl.P, &k, &smem);
+        KFP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0, dev = 0, sms = 0;
+        KFP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, pl.P * kfp::kWarp, smem));
+        KFP_CUDA(cudaGetDevice(&dev));
+        KFP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (per_sm < 1) {
+            set_err("column kernel: no CTA of %d threads with %zu B smem fits on an SM", pl.P * kfp::kWarp, smem);
+            return KFP_E_CUDA;
+        }
+        pl.Gc_total = per_sm * sms;
+        return KFP_OK;
+    }
     if (pl.window) {
         WindowKernel k;
         size_t smem;
@@ -799,7 +990,7 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     sd.slab[0] = pb->d_mono[0];
     sd.slab[1] = pb->d_mono[1];
     woodbury(pb, sd, 0.0);
-    Plan pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true);
+    Plan pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true, false, pb->nx);
     sd.nblk = (sd.n + pl.R - 1) / pl.R;
     if (kfp_status st = ensure_qtab(pb, std::max(pl.R, sd.n) + 2)) return st;
     if (kfp_status st = configure_kernels(pl)) return st;
@@ -822,6 +1013,7 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     if (!st) st = build_tmaps(pb, pl, std::vector<SubDev>{sd}, &fd.maps, &tmp2);
     if (!st) st = build_l2m(pb, pl, std::vector<SubDev>{sd}, &fd.l2c, &tmp2);
     if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &fd.coefT, &fd.tabs, &tmp2);
+    if (!st) st = build_col_tables(pb, pl, std::vector<SubDev>{sd}, &fd, &tmp2);
     if (!st && !rec_rows.empty()) {
         if (cudaMalloc(&d_rec, sizeof(int) * rec_rows.size()) != cudaSuccess ||
             cudaMemcpy(d_rec, rec_rows.data(), sizeof(int) * rec_rows.size(), cudaMemcpyHostToDevice) != cudaSuccess)
@@ -1087,7 +1279,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
     }
     std::vector<int> ns;
     for (const SubDev &sd : pb->subs) ns.push_back(sd.n);
-    pb->plan = make_plan(ns, pb->f_rank, true, true);
+    pb->plan = make_plan(ns, pb->f_rank, true, true, pb->nx);
     Plan &pl = pb->plan;
     // the rows of each outgoing trace stencil must sit in one row block
     for (int i = 0; i < nloc; ++i) {
@@ -1170,6 +1362,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
         if (!st) st = build_l2m(pb, pl, pb->subs, &pb->fd.l2c, &own);
         if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &pb->fd.coefT, &pb->fd.tabs, &own);
         if (!st) st = build_window_tables(pb, pl, nloc, &pb->fd, &own);
+        if (!st) st = build_col_tables(pb, pl, pb->subs, &pb->fd, &own);
         for (void *q : own) pb->swr_allocs.push_back(static_cast<double *>(q));
         if (st) return st;
     }

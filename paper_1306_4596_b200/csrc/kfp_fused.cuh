@@ -221,6 +221,26 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define KFP_TT(e)
 #endif
 
+#ifdef KFP_TRACE
+// debug builds only: accumulated phase times (ns) of thread 0 of every CTA, [cta][64]
+#define KFP_WT_DECL unsigned long long wt_acc[10] = {0}, wt_last = 0;
+#define KFP_WT(k)                                              \
+    if (g_kfp_trace && threadIdx.x == 0) {                     \
+        const unsigned long long now_ = gtime();               \
+        if ((k) >= 0 && wt_last) wt_acc[(k)] += now_ - wt_last; \
+        wt_last = now_;                                        \
+    }
+#define KFP_WT_FLUSH                                                                                        \
+    if (g_kfp_trace && threadIdx.x == 0) {                                                                  \
+        const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; \
+        for (int i_ = 0; i_ < 10; ++i_) g_kfp_trace[cta * 64 + i_] = wt_acc[i_];                            \
+    }
+#else
+#define KFP_WT_DECL
+#define KFP_WT(k)
+#define KFP_WT_FLUSH
+#endif
+
 // --------------------------------------------------------------------------- the kernel
 template <int B, int NR, int P_>
 __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const FusedParams FP) {

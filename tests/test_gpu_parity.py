@@ -186,3 +186,39 @@ def test_c4_full_size_properties(kfp):
             assert (a <= UT[lo:hi + 1] + 1e-14).all()
     assert UT.min() >= 0.0
     assert np.all(np.diff(eI) <= 0.0) and np.all(eT <= eI * (1 + 1e-12))
+
+
+# The two alternative SWR kernels (opt-in): the persistent pipelined window kernel
+# (KFP_WINDOW=1, one launch per iteration, step flags between clusters) and the cluster-free
+# column-tile kernel (KFP_COL=1).  Same bar against the oracle; the plan string proves which ran.
+ALT = {"window": ("KFP_WINDOW", "window-pipelined"), "column": ("KFP_COL", "column-tile")}
+ALT_CASES = ["c0", "c1", "robin_ov3", "c4_small", "dirichlet_ov0", "ragged_dirichlet_ov"]
+
+
+@pytest.mark.parametrize("alt", list(ALT))
+@pytest.mark.parametrize("name", ALT_CASES)
+def test_alternative_kernels_vs_oracle(kfp, monkeypatch, alt, name):
+    env, tag = ALT[alt]
+    monkeypatch.setenv(env, "1")
+    run = CASES[name]
+    g = _gpu(kfp, run)
+    if run.grid.nx % 8 == 0 or alt == "window":
+        assert g["plan"].startswith(tag), g["plan"]
+    _compare(g, _oracle(run), f"{alt}:{name}")
+
+
+@pytest.mark.parametrize("alt", list(ALT))
+def test_alternative_kernels_c2_full_size(kfp, monkeypatch, alt):
+    """configs[2] at full size through each alternative kernel, against the mode-reduced oracle."""
+    from oracle.modal import modal_swr, realize
+
+    env, tag = ALT[alt]
+    monkeypatch.setenv(env, "1")
+    run = ki.config("c2")
+    g = _gpu(kfp, run)
+    assert g["plan"].startswith(tag), g["plan"]
+    m = modal_swr(run.grid, run.kind, run.p, run.overlap, run.n_sub, run.K)
+    for s in range(run.n_sub):
+        assert rel(g["uT_sub"][s], realize(m["c_sub"][s], run.grid.nx)) <= TOL, (alt, s)
+    assert rel(g["err_T"], m["err_T"]) <= TOL
+    assert rel(g["err_if"], m["err_if"]) <= TOL
