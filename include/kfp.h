@@ -110,6 +110,14 @@ kfp_status kfp_monodomain_solve(kfp_problem pb, double *uT);
 kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overlap, int32_t n_sub,
                          int32_t s_begin, int32_t s_end, int32_t K_max);
 
+/* Two-sided optimized SWR, OSWR(p, q) (Table 1): every right (hi) end
+ * imposes (p + d_v) u = g and every left (lo) end (q - d_v) u = g, with the half-cell rows and
+ * traces of DESIGN.md R11; the trace a subdomain sends to its left neighbour uses p, the one it
+ * sends right uses q.  p, q > 0 for KFP_ROBIN (ignored for KFP_DIRICHLET); q = p is
+ * kfp_swr_setup.  Other arguments, ownership and errors as kfp_swr_setup. */
+kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, int32_t overlap, int32_t n_sub,
+                            int32_t s_begin, int32_t s_end, int32_t K_max);
+
 /* Reset to iteration 0: zero incoming traces (the initial guess) and
  * clear the error history. */
 kfp_status kfp_swr_reset(kfp_problem pb);
@@ -145,6 +153,10 @@ kfp_status kfp_swr_bind_edge_buffers(kfp_problem pb, int32_t parity, double *sen
  * n_sub-1), or NULL. */
 kfp_status kfp_swr_solve(kfp_problem pb, kfp_kind kind, double p, int32_t overlap, int32_t n_sub, int32_t K,
                          double *uT);
+
+/* kfp_swr_solve with OSWR(p, q) (see kfp_swr_setup_pq). */
+kfp_status kfp_swr_solve_pq(kfp_problem pb, kfp_kind kind, double p, double q, int32_t overlap, int32_t n_sub,
+                            int32_t K, double *uT);
 
 /* Error history of the iterations run since the last reset, from the local
  * block: err_T[k-1] = max_{s,m, j in [lo_s,hi_s]} |u_s^k(T) - U(T)|,

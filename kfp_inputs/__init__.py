@@ -109,6 +109,7 @@ class Run:
     overlap: int
     n_sub: int
     K: int
+    q: Optional[float] = None  # two-sided OSWR(p, q): Robin parameter of the left ends (None: q = p)
 
     @property
     def updates(self) -> int:

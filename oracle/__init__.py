@@ -72,6 +72,11 @@ def _load():
                                        ctypes.c_int, dp, dp, dp]
             lib.orc_swr.argtypes = [P, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     dp, dp, dp, dp, dp, dp]
+            lib.orc_swr_pq.argtypes = [P, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, dp, dp, dp, dp, dp, dp]
+            lib.orc_window_pq.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                          ctypes.c_double, dp, dp, ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, dp,
+                                          ctypes.c_int, dp, dp, dp]
             _lib = lib
     return _lib
 
@@ -117,8 +122,9 @@ def monodomain(prob, rec_nodes=()):
     return UT, rec[: len(nodes)]
 
 
-def window(prob, lo, hi, ltype, rtype, p, gL, gR, send_kind, sendL_node=-1, sendR_node=-1, rec_nodes=()):
-    """One subdomain window solve; returns (uT, sendL, sendR, rec)."""
+def window(prob, lo, hi, ltype, rtype, p, gL, gR, send_kind, sendL_node=-1, sendR_node=-1, rec_nodes=(), q=None):
+    """One subdomain window solve; returns (uT, sendL, sendR, rec).  Robin ends: p on the right (hi) end and
+    on the trace sent left, q (default p) on the left (lo) end and on the trace sent right (OSWR(p,q))."""
     g = prob.grid
     b = _Bound(prob)
     gL = None if gL is None else np.ascontiguousarray(gL, dtype=np.float64)
@@ -128,13 +134,15 @@ def window(prob, lo, hi, ltype, rtype, p, gL, gR, send_kind, sendL_node=-1, send
     nodes = np.ascontiguousarray(rec_nodes, dtype=np.int32)
     rec = np.zeros((max(len(nodes), 1), g.nt, g.nx))
     uT = np.zeros((hi - lo + 1, g.nx))
-    _load().orc_window(b.ref(), lo, hi, ltype, rtype, p, _ptr(gL), _ptr(gR), KIND[send_kind] if isinstance(send_kind, str) else send_kind,
-                       sendL_node, _ptr(sendL), sendR_node, _ptr(sendR), len(nodes), _ptr(nodes), _ptr(rec), _ptr(uT))
+    _load().orc_window_pq(b.ref(), lo, hi, ltype, rtype, p if q is None else q, p, _ptr(gL), _ptr(gR),
+                          KIND[send_kind] if isinstance(send_kind, str) else send_kind,
+                          sendL_node, _ptr(sendL), sendR_node, _ptr(sendR), len(nodes), _ptr(nodes), _ptr(rec), _ptr(uT))
     return uT, sendL, sendR, rec[: len(nodes)]
 
 
-def swr(prob, kind: str, p: float, overlap: int, n_sub: int, K: int, want_traces: bool = False):
-    """Jacobi SWR; returns dict(uT, uT_sub (list of slabs), UT, err_T, err_if, traces, lo, hi)."""
+def swr(prob, kind: str, p: float, overlap: int, n_sub: int, K: int, want_traces: bool = False, q=None):
+    """Jacobi SWR; returns dict(uT, uT_sub (list of slabs), UT, err_T, err_if, traces, lo, hi).
+    Robin: OSWR(p, q) with p on every right end and q (default p: one-sided OSWR(p)) on every left end."""
     g = prob.grid
     b = _Bound(prob)
     lo, hi = subdomains(g.nv, n_sub, overlap)
@@ -145,8 +153,8 @@ def swr(prob, kind: str, p: float, overlap: int, n_sub: int, K: int, want_traces
     err_T = np.zeros(K)
     err_if = np.zeros(K)
     traces = np.zeros((max(2 * (n_sub - 1), 1), g.nt, g.nx)) if want_traces else None
-    rc = _load().orc_swr(b.ref(), KIND[kind], p, overlap, n_sub, K, _ptr(uT_sub), _ptr(uT), _ptr(UT),
-                         _ptr(err_T), _ptr(err_if), _ptr(traces))
+    rc = _load().orc_swr_pq(b.ref(), KIND[kind], p, p if q is None else q, overlap, n_sub, K, _ptr(uT_sub),
+                            _ptr(uT), _ptr(UT), _ptr(err_T), _ptr(err_if), _ptr(traces))
     if rc != 0:
         raise ValueError("orc_swr rejected the arguments")
     slabs, off = [], 0

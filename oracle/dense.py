@@ -18,12 +18,13 @@ import numpy as np
 __all__ = ["dense_window", "dense_monodomain"]
 
 
-def dense_window(prob, lo, hi, lkind="phys", rkind="phys", p=0.0, gL=None, gR=None):
+def dense_window(prob, lo, hi, lkind="phys", rkind="phys", p=0.0, gL=None, gR=None, q=None):
     """Solve the space-time system of subdomain [lo, hi]; returns u [(nt+1), (hi-lo+1), nx].
 
     lkind/rkind: 'phys' (Dirichlet 0), 'dirichlet' (value = trace), 'robin'
-    ((p -/+ d_v) u = trace with the half-cell row).  gL/gR: [nt, nx] traces
-    (row n-1 = t_n)."""
+    ((q - d_v) u = trace at the left end, (p + d_v) u = trace at the right end, half-cell rows;
+    q defaults to p).  gL/gR: [nt, nx] traces (row n-1 = t_n)."""
+    pl = p if q is None else q
     g = prob.grid
     nx, nt = g.nx, g.nt
     hx, hv, dt = 1.0 / nx, 2.0 * g.vmax / g.nv, g.t_final / nt
@@ -58,7 +59,7 @@ def dense_window(prob, lo, hi, lkind="phys", rkind="phys", p=0.0, gL=None, gR=No
                 cl, cr = -a, -a
                 rhs = dt * f[j, m]
                 if j == lo and lkind == "robin":
-                    diag += 2.0 * a * p * hv
+                    diag += 2.0 * a * pl * hv
                     cr = -2.0 * a
                     cl = 0.0
                     rhs += 2.0 * a * hv * gL[n - 1, m]

@@ -99,8 +99,12 @@ static void thomas(int n, const double *sub, const double *diag, const double *s
  * (one solve of SWR1 / SWR3, with the Jacobi data of P:594-597).
  *
  *  ltype/rtype : END_PHYS | END_DIRICHLET | END_ROBIN for the end nodes lo/hi.
- *  p           : Robin parameter, used when an end is END_ROBIN or
- *                when send_kind == KIND_ROBIN.
+ *  pl, pr      : Robin parameters of the lo (left) and hi (right) ends:
+ *                the left end imposes (pl - d_v) u = g, the right end (pr + d_v) u = g.
+ *                Two-sided OSWR(p,q): every right end uses p and every
+ *                left end q, so pr = p, pl = q for all subdomains; one-sided OSWR(p):
+ *                pl = pr = p.  The trace sent to the left neighbour lands on its
+ *                right end and uses pr; the one sent right uses pl.
  *  gL, gR      : incoming traces [nt][nx] for the lo / hi end (NULL if physical).
  *  send_kind   : KIND_DIRICHLET or KIND_ROBIN, the kind of the outgoing traces.
  *  sendL_node  : node whose trace is sent to the left neighbour (its hi end),
@@ -111,7 +115,7 @@ static void thomas(int n, const double *sub, const double *diag, const double *s
  *                rec[i][n-1][m] (used for the interface error and U-lines).
  *  uT          : [(hi-lo+1)][nx] solution at t = T (may be NULL).
  */
-static void window(const orc_problem *P, int lo, int hi, int ltype, int rtype, double p,
+static void window(const orc_problem *P, int lo, int hi, int ltype, int rtype, double pl, double pr,
                    const double *gL, const double *gR, int send_kind,
                    int sendL_node, double *sendL, int sendR_node, double *sendR,
                    int nrec, const int *rec_nodes, double *rec, double *uT) {
@@ -168,15 +172,15 @@ static void window(const orc_problem *P, int lo, int hi, int ltype, int rtype, d
                     diag[i] = 1.0 + 2.0 * a;
                     sup[i] = -a;
                     rhs[i] = r[j - lo];
-                    if (j == lo) { /* Robin left end: (p - d_v) u = g, half-cell row (R11, R13) */
-                        diag[i] = 1.0 + 2.0 * a + 2.0 * a * p * hv;
+                    if (j == lo) { /* Robin left end: (pl - d_v) u = g, half-cell row (R11, R13) */
+                        diag[i] = 1.0 + 2.0 * a + 2.0 * a * pl * hv;
                         sup[i] = -2.0 * a;
                         rhs[i] += 2.0 * a * hv * gL[(size_t)n * nx + m];
                     } else if (j == lo + 1) { /* known node lo moved to the RHS (R10) */
                         rhs[i] += a * left_val;
                     }
-                    if (j == hi) { /* Robin right end: (p + d_v) u = g */
-                        diag[i] = 1.0 + 2.0 * a + 2.0 * a * p * hv;
+                    if (j == hi) { /* Robin right end: (pr + d_v) u = g */
+                        diag[i] = 1.0 + 2.0 * a + 2.0 * a * pr * hv;
                         sub[i] = -2.0 * a;
                         rhs[i] += 2.0 * a * hv * gR[(size_t)n * nx + m];
                     } else if (j == hi - 1) {
@@ -202,9 +206,9 @@ static void window(const orc_problem *P, int lo, int hi, int ltype, int rtype, d
             for (int m = 0; m < nx; ++m) {
                 double g;
                 if (send_kind == KIND_DIRICHLET) g = uc[m];
-                else { /* (p + d_v) u at node c, d_v u = half-cell flux on [c, c + h/2] */
+                else { /* (pr + d_v) u at node c, d_v u = half-cell flux on [c, c + h/2] */
                     const double ucp = uc[m + nx]; /* node c+1 */
-                    g = p * uc[m] - ((uc[m] - ucp) / hv + 0.5 * hv * (uc[m] - rL[m]) / dt);
+                    g = pr * uc[m] - ((uc[m] - ucp) / hv + 0.5 * hv * (uc[m] - rL[m]) / dt);
                 }
                 sendL[(size_t)n * nx + m] = g;
             }
@@ -214,9 +218,9 @@ static void window(const orc_problem *P, int lo, int hi, int ltype, int rtype, d
             for (int m = 0; m < nx; ++m) {
                 double g;
                 if (send_kind == KIND_DIRICHLET) g = uc[m];
-                else { /* (p - d_v) u at node c, d_v u = half-cell flux on [c - h/2, c] */
+                else { /* (pl - d_v) u at node c, d_v u = half-cell flux on [c - h/2, c] */
                     const double ucm = uc[m - nx]; /* node c-1 */
-                    g = p * uc[m] - ((uc[m] - ucm) / hv + 0.5 * hv * (uc[m] - rR[m]) / dt);
+                    g = pl * uc[m] - ((uc[m] - ucm) / hv + 0.5 * hv * (uc[m] - rR[m]) / dt);
                 }
                 sendR[(size_t)n * nx + m] = g;
             }
@@ -261,30 +265,40 @@ int orc_subdomains(int nv, int n_sub, int overlap, int32_t *lo, int32_t *hi) {
 int orc_monodomain(const orc_problem *P, int nrec, const int32_t *rec_nodes, double *rec, double *UT) {
     int *nodes = (int *)malloc(sizeof(int) * (nrec > 0 ? nrec : 1));
     for (int i = 0; i < nrec; ++i) nodes[i] = rec_nodes[i];
-    window(P, 0, P->nv, END_PHYS, END_PHYS, 0.0, NULL, NULL, KIND_DIRICHLET, -1, NULL, -1, NULL,
+    window(P, 0, P->nv, END_PHYS, END_PHYS, 0.0, 0.0, NULL, NULL, KIND_DIRICHLET, -1, NULL, -1, NULL,
            nrec, nodes, rec, UT);
     free(nodes);
     return 0;
 }
 
 /* One subdomain window with explicit ends and traces (used by the tests'
- * distributed-driver backend).  Arguments as in window(). */
+ * distributed-driver backend).  Arguments as in window(); orc_window is the
+ * one-sided form pl = pr = p. */
+int orc_window_pq(const orc_problem *P, int lo, int hi, int ltype, int rtype, double pl, double pr,
+                  const double *gL, const double *gR, int send_kind,
+                  int sendL_node, double *sendL, int sendR_node, double *sendR,
+                  int nrec, const int32_t *rec_nodes, double *rec, double *uT) {
+    int *nodes = (int *)malloc(sizeof(int) * (nrec > 0 ? nrec : 1));
+    for (int i = 0; i < nrec; ++i) nodes[i] = rec_nodes[i];
+    window(P, lo, hi, ltype, rtype, pl, pr, gL, gR, send_kind, sendL_node, sendL, sendR_node, sendR,
+           nrec, nodes, rec, uT);
+    free(nodes);
+    return 0;
+}
 int orc_window(const orc_problem *P, int lo, int hi, int ltype, int rtype, double p,
                const double *gL, const double *gR, int send_kind,
                int sendL_node, double *sendL, int sendR_node, double *sendR,
                int nrec, const int32_t *rec_nodes, double *rec, double *uT) {
-    int *nodes = (int *)malloc(sizeof(int) * (nrec > 0 ? nrec : 1));
-    for (int i = 0; i < nrec; ++i) nodes[i] = rec_nodes[i];
-    window(P, lo, hi, ltype, rtype, p, gL, gR, send_kind, sendL_node, sendL, sendR_node, sendR,
-           nrec, nodes, rec, uT);
-    free(nodes);
-    return 0;
+    return orc_window_pq(P, lo, hi, ltype, rtype, p, p, gL, gR, send_kind, sendL_node, sendL, sendR_node, sendR,
+                         nrec, rec_nodes, rec, uT);
 }
 
 /* Jacobi SWR (P:554-597 with the Remark at P:594-597), K iterations from zero
  * traces, errors against the monodomain solution.
  *
- *  kind        : KIND_DIRICHLET (CSWR, Q = identity) or KIND_ROBIN (OSWR(p), p = q).
+ *  kind        : KIND_DIRICHLET (CSWR, Q = identity) or KIND_ROBIN: OSWR(p, q) with p on
+ *                every right (hi) end and q on every left (lo) end;
+ *                orc_swr is the one-sided OSWR(p), q = p.
  *  uT_sub      : concatenated per-subdomain slabs u_s^K(T), s = 0..S-1 (may be NULL).
  *  uT          : [(nv+1)][nx] assembled by nominal ownership (node j belongs to
  *                the s with c_s <= j < c_{s+1}; node nv to S-1) (may be NULL).
@@ -295,8 +309,8 @@ int orc_window(const orc_problem *P, int lo, int hi, int ltype, int rtype, doubl
  *                (between s=i and s=i+1) first toLeft[i] (sent by i+1, used at hi_i)
  *                then toRight[i] (sent by i, used at lo_{i+1}); may be NULL.
  */
-int orc_swr(const orc_problem *P, int kind, double p, int overlap, int n_sub, int K,
-            double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
+int orc_swr_pq(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K,
+               double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
     const int nx = P->nx, nt = P->nt, nv = P->nv, S = n_sub;
     if (S < 1 || nv % S != 0 || K < 1) return -1;
     int32_t *lo = (int32_t *)malloc(sizeof(int32_t) * S), *hi = (int32_t *)malloc(sizeof(int32_t) * S);
@@ -339,7 +353,7 @@ int orc_swr(const orc_problem *P, int kind, double p, int overlap, int n_sub, in
             if (s > 0) { rn[nrec] = lo[s]; lidx[nrec++] = lo[s]; }
             if (s < S - 1) { rn[nrec] = hi[s]; lidx[nrec++] = hi[s]; }
             double *us = slabs + off;
-            window(P, lo[s], hi[s], lt, rt, p, gL, gR, kind,
+            window(P, lo[s], hi[s], lt, rt, q, p, gL, gR, kind,
                    sendL, (s > 0) ? toL_out + (size_t)(s - 1) * TR : NULL,
                    sendR, (s < S - 1) ? toR_out + (size_t)s * TR : NULL, nrec, rn, rec, us);
             /* interface error (all steps n = 1..nt) */
@@ -383,4 +397,8 @@ int orc_swr(const orc_problem *P, int kind, double p, int overlap, int n_sub, in
     free(lo); free(hi); free(lines); free(Ulines); free(Ut);
     free(toL_in); free(toR_in); free(toL_out); free(toR_out); free(slabs); free(rec);
     return 0;
+}
+int orc_swr(const orc_problem *P, int kind, double p, int overlap, int n_sub, int K,
+            double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
+    return orc_swr_pq(P, kind, p, p, overlap, n_sub, K, uT_sub, uT, UT, err_T, err_if, traces);
 }

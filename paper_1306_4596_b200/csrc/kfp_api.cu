@@ -318,7 +318,7 @@ struct kfp_problem_s {
     // SWR
     bool setup = false;
     int kind = 0;
-    double p = 0;
+    double p = 0, q_rob = 0;  // Robin parameters: p on right (hi) ends, q_rob on left (lo) ends
     int ov = 0, S = 0, s_begin = 0, s_end = 0, K_max = 0, k_done = 0;
     std::vector<int> lo, hi;
     std::vector<SubDev> subs;  // local block
@@ -386,13 +386,14 @@ void decompose(int nv, int S, int ov, std::vector<int> &lo, std::vector<int> &hi
 }
 
 // Woodbury constants of one column system.
-void woodbury(const kfp_problem pb, SubDev &sd, double p) {
+// pl, pr: Robin parameters of the lo (left) and hi (right) end rows (OSWR(p, q): pl = q, pr = p).
+void woodbury(const kfp_problem pb, SubDev &sd, double pl, double pr) {
     const long double a = pb->a, q = pb->q, h = pb->hv;
     const int n = sd.n;
     // d_t on rows (0,1), d_b on rows (n-2, n-1)
     long double wt0, wt1, wb0, wb1;
     if (sd.ltype == kfp::END_ROBIN) {
-        wt0 = a * (2.0L * p * h + q);
+        wt0 = a * (2.0L * pl * h + q);
         wt1 = -a;
     } else {
         wt0 = a * q;
@@ -400,7 +401,7 @@ void woodbury(const kfp_problem pb, SubDev &sd, double p) {
     }
     if (sd.rtype == kfp::END_ROBIN) {
         wb0 = -a;
-        wb1 = 2.0L * a * p * h;
+        wb1 = 2.0L * a * pr * h;
     } else {
         wb0 = 0.0L;
         wb1 = 0.0L;
@@ -989,7 +990,7 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     sd.ifL = sd.ifR = -1;
     sd.slab[0] = pb->d_mono[0];
     sd.slab[1] = pb->d_mono[1];
-    woodbury(pb, sd, 0.0);
+    woodbury(pb, sd, 0.0, 0.0);
     Plan pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true, false, pb->nx);
     sd.nblk = (sd.n + pl.R - 1) / pl.R;
     if (kfp_status st = ensure_qtab(pb, std::max(pl.R, sd.n) + 2)) return st;
@@ -1177,6 +1178,11 @@ kfp_status kfp_monodomain_uT(kfp_problem pb, double *out) {
 
 kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overlap, int32_t n_sub, int32_t s_begin,
                          int32_t s_end, int32_t K_max) {
+    return kfp_swr_setup_pq(pb, kind, p, p, overlap, n_sub, s_begin, s_end, K_max);
+}
+
+kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, int32_t overlap, int32_t n_sub,
+                            int32_t s_begin, int32_t s_end, int32_t K_max) {
     if (!pb) {
         set_err("kfp_swr_setup: NULL problem");
         return KFP_E_INVAL;
@@ -1185,8 +1191,8 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
         set_err("kfp_swr_setup: unknown kind %d", (int)kind);
         return KFP_E_INVAL;
     }
-    if (kind == KFP_ROBIN && !(p > 0)) {
-        set_err("kfp_swr_setup: Robin parameter p must be > 0 (P:58), got %g", p);
+    if (kind == KFP_ROBIN && !(p > 0 && q > 0)) {
+        set_err("kfp_swr_setup: Robin parameters p, q must be > 0 (P:58), got %g, %g", p, q);
         return KFP_E_INVAL;
     }
     if (n_sub < 1 || pb->nv % n_sub != 0) {
@@ -1215,6 +1221,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
 
     pb->kind = kind;
     pb->p = p;
+    pb->q_rob = (kind == KFP_ROBIN) ? q : p;
     pb->ov = overlap;
     pb->S = n_sub;
     pb->s_begin = s_begin;
@@ -1274,7 +1281,7 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
             set_err("kfp_swr_setup: subdomain %d has %d unknown rows (need >= 2)", s, sd.n);
             return KFP_E_INVAL;
         }
-        woodbury(pb, sd, p);
+        woodbury(pb, sd, pb->q_rob, p);
         n_max = std::max(n_max, sd.n);
     }
     std::vector<int> ns;
@@ -1412,6 +1419,7 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
     P.subs = pb->d_subs;
     P.send_robin = (pb->kind == KFP_ROBIN);
     P.p = pb->p;
+    P.q_lo = pb->q_rob;
     P.UT = pb->d_UT;
     P.Ulines = pb->d_Ulines;
     P.blkagg = pb->d_blkagg;
@@ -1497,7 +1505,12 @@ kfp_status kfp_swr_bind_edge_buffers(kfp_problem pb, int32_t parity, double *sen
 
 kfp_status kfp_swr_solve(kfp_problem pb, kfp_kind kind, double p, int32_t overlap, int32_t n_sub, int32_t K,
                          double *uT) {
-    if (kfp_status st = kfp_swr_setup(pb, kind, p, overlap, n_sub, 0, n_sub, K)) return st;
+    return kfp_swr_solve_pq(pb, kind, p, p, overlap, n_sub, K, uT);
+}
+
+kfp_status kfp_swr_solve_pq(kfp_problem pb, kfp_kind kind, double p, double q, int32_t overlap, int32_t n_sub,
+                            int32_t K, double *uT) {
+    if (kfp_status st = kfp_swr_setup_pq(pb, kind, p, q, overlap, n_sub, 0, n_sub, K)) return st;
     std::string warn = g_err;
     if (kfp_status st = kfp_swr_iterate(pb, K)) return st;
     if (uT) {
@@ -1599,6 +1612,7 @@ extern "C" int kfp_debug_trace_step(kfp_problem pb, int n, unsigned long long *h
     P.subs = pb->d_subs;
     P.send_robin = (pb->kind == KFP_ROBIN);
     P.p = pb->p;
+    P.q_lo = pb->q_rob;
     P.UT = pb->d_UT;
     P.Ulines = pb->d_Ulines;
     P.errT = pb->d_errT;

@@ -72,6 +72,8 @@ struct StepParams {
     int qtab_len;
     int record;            // monodomain: record rows listed in line_of_node
     double q, a, qa, hv, dt, p;
+    double q_lo;           // Robin parameter of the left (lo) ends: q of OSWR(p, q) (= p for OSWR(p)); the
+                           // trace sent RIGHT lands on a left end and uses q_lo, the one sent left uses p
     double cf[kMaxRank];   // dt * ft[r][n+1]
     const double2 *rowc;   // per node: (1-|nu_j|, |nu_j|)
     const double *fv;      // [f_rank][nv+1]
@@ -509,9 +511,9 @@ __device__ __forceinline__ void write_traces(const StepParams &P, const Tile &t,
     if (S.iR_tr >= 0 && S.iR_tr >= t.rb0 && S.iR_tr < t.rb0 + t.Rb) {
         const double uc = xtr[2 * kWarp + t.lane];
         double g = uc;
-        if (P.send_robin) {  // (p - d_v) u with the half-cell flux on [c-h/2, c]
+        if (P.send_robin) {  // (q - d_v) u with the half-cell flux on [c-h/2, c]
             const double um = xtr[3 * kWarp + t.lane];
-            g = P.p * uc - ((uc - um) * inv_h + half_h_dt * (uc - rtr[kWarp + t.lane]));
+            g = P.q_lo * uc - ((uc - um) * inv_h + half_h_dt * (uc - rtr[kWarp + t.lane]));
         }
         S.sendR[P.par_out][off] = g;
     }

@@ -456,11 +456,11 @@ __global__ void __launch_bounds__(P_ * kWarp, 1) step_window(const WinParams W) 
                 if (P.send_robin) g = P.p * uc - ((uc - sm.xsp[kWarp + lane]) * inv_h + half_h_dt * (uc - rtr[lane]));
                 S.sendL[P.par_out][goff] = g;
             }
-            if (tr_R && inblk(S.iR_tr)) {  // (p - d_v) u at lo_{s+1}, flux on [c-h/2, c]
+            if (tr_R && inblk(S.iR_tr)) {  // (q - d_v) u at lo_{s+1}, flux on [c-h/2, c]
                 const double uc = sm.xsp[2 * kWarp + lane];
                 double g = uc;
                 if (P.send_robin)
-                    g = P.p * uc - ((uc - sm.xsp[3 * kWarp + lane]) * inv_h + half_h_dt * (uc - rtr[kWarp + lane]));
+                    g = P.q_lo * uc - ((uc - sm.xsp[3 * kWarp + lane]) * inv_h + half_h_dt * (uc - rtr[kWarp + lane]));
                 S.sendR[P.par_out][goff] = g;
             }
             if (inblk(sp_row[4]))

@@ -36,7 +36,7 @@ class CudaBlock:
     """The local block on this rank's GPU, through the C-ABI (libkfp.so)."""
 
     def __init__(self, prob, kind: str, p: float, overlap: int, n_sub: int, K: int, rank: int, world: int,
-                 device: int):
+                 device: int, q=None):
         from .kfp import Problem
 
         self.s_begin, self.s_end = block_of(rank, world, n_sub)
@@ -46,7 +46,7 @@ class CudaBlock:
         self.stream = torch.cuda.current_stream()
         self.pb = Problem(prob, device=device)
         self.pb.set_stream(self.stream.cuda_stream)
-        self.pb.setup(kind, p, overlap, n_sub, K, self.s_begin, self.s_end)
+        self.pb.setup(kind, p, overlap, n_sub, K, self.s_begin, self.s_end, q=q)
         shape = (g.nt, g.nx)
         mk = lambda: torch.zeros(shape, dtype=torch.float64, device=f"cuda:{device}")
         self.has_left, self.has_right = self.s_begin > 0, self.s_end < n_sub

@@ -20,7 +20,7 @@ KIND = {"dirichlet": 0, "robin": 1}
 
 # Every symbol include/kfp.h declares (checked by tests/test_abi.py).
 SYMBOLS = (
-    "kfp_problem_create", "kfp_problem_destroy", "kfp_set_stream", "kfp_monodomain_solve", "kfp_swr_setup",
+    "kfp_problem_create", "kfp_problem_destroy", "kfp_set_stream", "kfp_monodomain_solve", "kfp_swr_setup", "kfp_swr_setup_pq", "kfp_swr_solve_pq",
     "kfp_swr_reset", "kfp_swr_iterate", "kfp_swr_edge_buffers", "kfp_swr_bind_edge_buffers", "kfp_swr_solve", "kfp_error_history",
     "kfp_swr_subdomain_uT", "kfp_swr_subdomain_range", "kfp_swr_trace", "kfp_monodomain_uT", "kfp_launch_count",
     "kfp_plan", "kfp_last_timing", "kfp_last_error",
@@ -66,6 +66,8 @@ def load(path: str = LIB_PATH):
         "kfp_set_stream": (i32, [vp, vp]),
         "kfp_monodomain_solve": (i32, [vp, vp]),
         "kfp_swr_setup": (i32, [vp, i32, dbl, i32, i32, i32, i32, i32]),
+        "kfp_swr_setup_pq": (i32, [vp, i32, dbl, dbl, i32, i32, i32, i32, i32]),
+        "kfp_swr_solve_pq": (i32, [vp, i32, dbl, dbl, i32, i32, i32, vp]),
         "kfp_swr_reset": (i32, [vp]),
         "kfp_swr_iterate": (i32, [vp, i32]),
         "kfp_swr_edge_buffers": (i32, [vp, i32, ppd, ppd, ppd, ppd]),
@@ -152,10 +154,15 @@ class Problem:
         return out
 
     def setup(self, kind: str, p: float, overlap: int, n_sub: int, K_max: int, s_begin: int = 0,
-              s_end: Optional[int] = None):
+              s_end: Optional[int] = None, q: Optional[float] = None):
+        """q: Robin parameter of the left ends (two-sided OSWR(p, q)); None = one-sided OSWR(p)."""
         s_end = n_sub if s_end is None else s_end
-        _check(load().kfp_swr_setup(self._h, KIND[kind], float(p), int(overlap), int(n_sub), int(s_begin),
-                                    int(s_end), int(K_max)))
+        if q is None:
+            _check(load().kfp_swr_setup(self._h, KIND[kind], float(p), int(overlap), int(n_sub), int(s_begin),
+                                        int(s_end), int(K_max)))
+        else:
+            _check(load().kfp_swr_setup_pq(self._h, KIND[kind], float(p), float(q), int(overlap), int(n_sub),
+                                           int(s_begin), int(s_end), int(K_max)))
         self.n_sub, self.s_begin, self.s_end = n_sub, s_begin, s_end
 
     def reset(self):
@@ -176,10 +183,15 @@ class Problem:
         _check(load().kfp_swr_bind_edge_buffers(self._h, int(parity), c(send_left), c(recv_left), c(send_right),
                                                 c(recv_right)))
 
-    def solve(self, kind: str, p: float, overlap: int, n_sub: int, K: int, copy: bool = True):
+    def solve(self, kind: str, p: float, overlap: int, n_sub: int, K: int, copy: bool = True,
+              q: Optional[float] = None):
         g = self.grid
         out = np.empty((g.nv + 1, g.nx)) if copy else None
-        _check(load().kfp_swr_solve(self._h, KIND[kind], float(p), int(overlap), int(n_sub), int(K), _ptr(out)))
+        if q is None:
+            _check(load().kfp_swr_solve(self._h, KIND[kind], float(p), int(overlap), int(n_sub), int(K), _ptr(out)))
+        else:
+            _check(load().kfp_swr_solve_pq(self._h, KIND[kind], float(p), float(q), int(overlap), int(n_sub), int(K),
+                                           _ptr(out)))
         self.n_sub, self.s_begin, self.s_end = n_sub, 0, n_sub
         return out
 

@@ -22,6 +22,8 @@ import kfp_inputs as ki
 RUNS = {
     "robin4": ki.scaled(ki.config("c3"), nx=16, nv=64, nt=30, K=5).with_(n_sub=4),
     "dirichlet4": ki.scaled(ki.config("c4"), nx=16, nv=64, nt=30, K=5).with_(n_sub=4, overlap=4),
+    # two-sided OSWR(p, q): the traces that cross the rank boundary carry q one way and p the other
+    "robin_pq4": ki.scaled(ki.config("c3"), nx=16, nv=64, nt=30, K=5).with_(n_sub=4, p=3.0, q=0.8),
 }
 
 
@@ -80,7 +82,7 @@ class OracleBlock:
             rec = [n for n in ((lo,) if s > 0 else ()) + ((hi,) if s < S - 1 else ())]
             uT, sL, sR, r = o.window(self.prob, lo, hi, o.END_PHYS if s == 0 else et, o.END_PHYS if s == S - 1 else et,
                                      run.p, gL, gR, run.kind, int(self.hi[s - 1]) if s > 0 else -1,
-                                     int(self.lo[s + 1]) if s < S - 1 else -1, rec_nodes=rec)
+                                     int(self.lo[s + 1]) if s < S - 1 else -1, rec_nodes=rec, q=run.q)
             if s > 0:
                 dst = self.send_left[pout] if s == self.s_begin else self.toL[s - 1][pout]
                 dst.copy_(torch.from_numpy(sL))
@@ -120,7 +122,7 @@ def _worker(rank, world, port, name, out):
 @pytest.mark.parametrize("name", list(RUNS))
 def test_two_rank_gloo_matches_single_process(orc, name):
     run = RUNS[name]
-    ref = orc.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, run.K)
+    ref = orc.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(2, _free_port(), name, out), nprocs=2, join=True)

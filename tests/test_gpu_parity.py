@@ -38,13 +38,13 @@ def kfp():
 def _oracle(run):
     import oracle
 
-    return oracle.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, run.K, want_traces=True)
+    return oracle.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, run.K, want_traces=True, q=run.q)
 
 
 def _gpu(kfp, run):
     prob = ki.make_problem(run)
     with kfp.Problem(prob) as pb:
-        uT = pb.solve(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        uT = pb.solve(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
         eT, eI = pb.history()
         slabs = [pb.subdomain_uT(s) for s in range(run.n_sub)]
         UT = pb.monodomain_uT()
@@ -83,6 +83,10 @@ CASES = {
     "c4_small": ki.scaled(ki.config("c4"), nx=64, nv=32 * 32, nt=60, K=6, name="c4_small"),
     # one subdomain (must equal the monodomain), several row blocks per column
     "single_sub": ki.scaled(ki.config("c0"), nv=1200, nt=100, name="single").with_(n_sub=1, K=1),
+    # two-sided OSWR(p, q): q on left ends, p on right ends
+    "oswr_pq": ki.config("c0").with_(name="oswr_pq", p=2.5, q=0.4, K=8),
+    "oswr_pq_ov_S4": ki.scaled(ki.config("c1"), nt=300, K=6, name="oswr_pq_ov").with_(
+        kind="robin", p=1.5, q=6.0, overlap=2, n_sub=4),
     # columns taller than one cluster -> three-phase path
     "three_phase": ki.scaled(ki.config("c2"), nx=64, nv=4400, nt=40, K=3, name="three_phase").with_(n_sub=1),
 }
@@ -192,7 +196,7 @@ def test_c4_full_size_properties(kfp):
 # (KFP_WINDOW=1, one launch per iteration, step flags between clusters) and the cluster-free
 # column-tile kernel (KFP_COL=1).  Same bar against the oracle; the plan string proves which ran.
 ALT = {"window": ("KFP_WINDOW", "window-pipelined"), "column": ("KFP_COL", "column-tile")}
-ALT_CASES = ["c0", "c1", "robin_ov3", "c4_small", "dirichlet_ov0", "ragged_dirichlet_ov"]
+ALT_CASES = ["c0", "c1", "robin_ov3", "c4_small", "dirichlet_ov0", "ragged_dirichlet_ov", "oswr_pq_ov_S4"]
 
 
 @pytest.mark.parametrize("alt", list(ALT))
