@@ -362,8 +362,11 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             } else if (m0 == 0 || m0 + w == P.nx) {
                 // periodic wrap of the halo at the ends of the x range (TMA zero-fills out-of-range columns)
                 const double *src = S.slab[P.n & 1] + static_cast<size_t>(S.first - S.lo + cr0) * P.nx;
-                if (m0 == 0 && lane < Lw) tile_w[lane * kTW + kHalo - 1] = src[static_cast<size_t>(lane) * P.nx + P.nx - 1];
-                if (m0 + w == P.nx && lane < Lw) tile_w[lane * kTW + kHalo + w] = src[static_cast<size_t>(lane) * P.nx];
+                // one row per lane, strided: a chunk may hold more rows (L <= 33) than a warp has lanes
+                for (int l = lane; l < Lw; l += kWarp) {
+                    if (m0 == 0) tile_w[l * kTW + kHalo - 1] = src[static_cast<size_t>(l) * P.nx + P.nx - 1];
+                    if (m0 + w == P.nx) tile_w[l * kTW + kHalo + w] = src[static_cast<size_t>(l) * P.nx];
+                }
                 __syncwarp();
             }
             const int jv2_0 = 2 * (S.first + cr0) - P.nv;      // 2 j - nv of the chunk's first row

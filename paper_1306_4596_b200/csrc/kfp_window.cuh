@@ -505,8 +505,10 @@ __global__ void __launch_bounds__(P_ * kWarp, 1) step_window(const WinParams W) 
                     // periodic wrap of the halo at the ends of the x range (TMA zero-fills out-of-range columns);
                     // L2 loads (.cg): this SM may hold a stale L1 line of the ping-pong slab
                     const double *src = S.slab[n & 1] + static_cast<size_t>(S.first - S.lo + cr0) * P.nx;
-                    if (m0 == 0 && lane < Lw) tile_w[lane * kTW + kHalo - 1] = __ldcg(src + static_cast<size_t>(lane) * P.nx + P.nx - 1);
-                    if (m0 + w == P.nx && lane < Lw) tile_w[lane * kTW + kHalo + w] = __ldcg(src + static_cast<size_t>(lane) * P.nx);
+                    for (int l = lane; l < Lw; l += kWarp) {  // strided: a chunk may hold 33 rows
+                        if (m0 == 0) tile_w[l * kTW + kHalo - 1] = __ldcg(src + static_cast<size_t>(l) * P.nx + P.nx - 1);
+                        if (m0 + w == P.nx) tile_w[l * kTW + kHalo + w] = __ldcg(src + static_cast<size_t>(l) * P.nx);
+                    }
                     __syncwarp();
                 }
             } else {  // u^0 from the separable u0 tables (0 B of HBM), incl. the halo columns

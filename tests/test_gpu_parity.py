@@ -87,6 +87,11 @@ CASES = {
     "oswr_pq": ki.config("c0").with_(name="oswr_pq", p=2.5, q=0.4, K=8),
     "oswr_pq_ov_S4": ki.scaled(ki.config("c1"), nt=300, K=6, name="oswr_pq_ov").with_(
         kind="robin", p=1.5, q=6.0, overlap=2, n_sub=4),
+    # 33-row chunks (B = 33, more rows than lanes): the periodic-halo patch of the x-boundary tiles must
+    # cover every row (regression: row 32 kept the TMA zero fill)
+    "chunk33_robin": ki.scaled(ki.config("c0"), nx=64, nv=520, nt=6, K=3, t_final=0.015, name="chunk33_robin"),
+    "chunk33_dirichlet": ki.scaled(ki.config("c0"), nx=96, nv=520, nt=6, K=3, t_final=0.015,
+                                   name="chunk33_dir").with_(kind="dirichlet", p=0.0, overlap=4),
     # columns taller than one cluster -> three-phase path
     "three_phase": ki.scaled(ki.config("c2"), nx=64, nv=4400, nt=40, K=3, name="three_phase").with_(n_sub=1),
 }
@@ -166,6 +171,25 @@ def test_c2_full_size_vs_mode_reduced_oracle(kfp):
     assert rel(g["err_if"], m["err_if"]) <= TOL
 
 
+def test_c3_full_size_vs_mode_reduced_oracle(kfp):
+    """BASELINE.json configs[3] (8 Robin subdomains of 2049 rows -- the 33-row chunks, B = 33 -- over
+    N_x = 8192) at full size on one GPU, K cut to 3, against the mode-reduced oracle: every element
+    of every subdomain slab and both error histories."""
+    from oracle.modal import modal_swr, realize
+
+    run = ki.config("c3").with_(K=3)
+    prob = ki.make_problem(run)
+    with kfp.Problem(prob) as pb:
+        pb.solve(run.kind, run.p, run.overlap, run.n_sub, run.K, copy=False)
+        eT, eI = pb.history()
+        plan = pb.plan()
+        m = modal_swr(run.grid, run.kind, run.p, run.overlap, run.n_sub, run.K)
+        for s in range(run.n_sub):
+            assert rel(pb.subdomain_uT(s), realize(m["c_sub"][s], run.grid.nx)) <= TOL, (s, plan)
+    assert "B=33" in plan, plan
+    assert rel(eT, m["err_T"]) <= TOL and rel(eI, m["err_if"]) <= TOL
+
+
 def test_c4_full_size_properties(kfp):
     """BASELINE.json configs[4] at full size on one GPU: discrete maximum principle and monotone
     Schwarz iterates hold at any size: 0 <= u^k <= U, err
@@ -196,7 +220,8 @@ def test_c4_full_size_properties(kfp):
 # (KFP_WINDOW=1, one launch per iteration, step flags between clusters) and the cluster-free
 # column-tile kernel (KFP_COL=1).  Same bar against the oracle; the plan string proves which ran.
 ALT = {"window": ("KFP_WINDOW", "window-pipelined"), "column": ("KFP_COL", "column-tile")}
-ALT_CASES = ["c0", "c1", "robin_ov3", "c4_small", "dirichlet_ov0", "ragged_dirichlet_ov", "oswr_pq_ov_S4"]
+ALT_CASES = ["c0", "c1", "robin_ov3", "c4_small", "dirichlet_ov0", "ragged_dirichlet_ov", "oswr_pq_ov_S4",
+             "chunk33_robin", "chunk33_dirichlet"]
 
 
 @pytest.mark.parametrize("alt", list(ALT))
