@@ -92,6 +92,10 @@ CASES = {
     "chunk33_robin": ki.scaled(ki.config("c0"), nx=64, nv=520, nt=6, K=3, t_final=0.015, name="chunk33_robin"),
     "chunk33_dirichlet": ki.scaled(ki.config("c0"), nx=96, nv=520, nt=6, K=3, t_final=0.015,
                                    name="chunk33_dir").with_(kind="dirichlet", p=0.0, overlap=4),
+    # the full column geometry of configs[3] and [4] (8 Robin subdomains of 2049 rows; 32 Dirichlet
+    # subdomains of 1029 rows with 4-cell overlap, random f >= 0), small x-extent and window
+    "c3_columns": ki.scaled(ki.config("c3"), nx=64, nt=16, K=2, t_final=0.02 * 16 / 1000 * 8, name="c3_columns"),
+    "c4_columns": ki.scaled(ki.config("c4"), nx=64, nt=16, K=3, name="c4_columns"),
     # columns taller than one cluster -> three-phase path
     "three_phase": ki.scaled(ki.config("c2"), nx=64, nv=4400, nt=40, K=3, name="three_phase").with_(n_sub=1),
 }
