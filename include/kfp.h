@@ -59,6 +59,11 @@ typedef enum {
     KFP_ROBIN = 1      /* optimised SWR OSWR(p): Q1 = p + d_v, Q2 = p - d_v (p = q) */
 } kfp_kind;
 
+typedef enum {
+    KFP_JACOBI = 0,      /* parallel schedule (Remark P:594-597) */
+    KFP_GAUSS_SEIDEL = 1 /* the paper's serial SWR1-SWR4 */
+} kfp_schedule;
+
 /* Problem description (PAPER.md:33-38 data f, u0, T; grid per DESIGN.md R5/R6).
  * f(t_n, x_m, v_j) = sum_{r<f_rank} ft[r*(nt+1)+n] * fv[r*(nv+1)+j] * fx[r*nx+m]
  * u0(x_m, v_j)     = sum_{r<u0_rank} u0v[r*(nv+1)+j] * u0x[r*nx+m]   (u0_rank = 0: u0 = 0)
@@ -117,6 +122,15 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
  * kfp_swr_setup.  Other arguments, ownership and errors as kfp_swr_setup. */
 kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, int32_t overlap, int32_t n_sub,
                             int32_t s_begin, int32_t s_end, int32_t K_max);
+
+/* Iteration schedule of the configured solve (default after every setup: KFP_JACOBI).
+ *  KFP_JACOBI       : every subdomain reads the traces of iteration k-1 (the parallel form, Remark P:594-597).
+ *  KFP_GAUSS_SEIDEL : the paper's SWR1-SWR4: the subdomains in increasing v, each reading the
+ *                     trace its left neighbour wrote in the same iteration and the right neighbour's of k-1.
+ *                     Needs all subdomains on this process (s_begin = 0, s_end = n_sub) and a per-step plan;
+ *                     KFP_E_INVAL otherwise.  For two subdomains from zero traces, iterate k of subdomain 0
+ *                     (1) equals Jacobi iterate 2k-1 (2k). */
+kfp_status kfp_swr_set_schedule(kfp_problem pb, kfp_schedule schedule);
 
 /* Reset to iteration 0: zero incoming traces (the initial guess) and
  * clear the error history. */

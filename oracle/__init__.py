@@ -74,6 +74,7 @@ def _load():
                                     dp, dp, dp, dp, dp, dp]
             lib.orc_swr_pq.argtypes = [P, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_int, dp, dp, dp, dp, dp, dp]
+            lib.orc_swr_gs.argtypes = lib.orc_swr_pq.argtypes
             lib.orc_window_pq.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                           ctypes.c_double, dp, dp, ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, dp,
                                           ctypes.c_int, dp, dp, dp]
@@ -140,9 +141,11 @@ def window(prob, lo, hi, ltype, rtype, p, gL, gR, send_kind, sendL_node=-1, send
     return uT, sendL, sendR, rec[: len(nodes)]
 
 
-def swr(prob, kind: str, p: float, overlap: int, n_sub: int, K: int, want_traces: bool = False, q=None):
+def swr(prob, kind: str, p: float, overlap: int, n_sub: int, K: int, want_traces: bool = False, q=None,
+        schedule: str = "jacobi"):
     """Jacobi SWR; returns dict(uT, uT_sub (list of slabs), UT, err_T, err_if, traces, lo, hi).
-    Robin: OSWR(p, q) with p on every right end and q (default p: one-sided OSWR(p)) on every left end."""
+    Robin: OSWR(p, q) with p on every right end and q (default p: one-sided OSWR(p)) on every left end.
+    schedule: "jacobi" (parallel) or "gauss_seidel" (the paper's SWR1-SWR4)."""
     g = prob.grid
     b = _Bound(prob)
     lo, hi = subdomains(g.nv, n_sub, overlap)
@@ -153,8 +156,9 @@ def swr(prob, kind: str, p: float, overlap: int, n_sub: int, K: int, want_traces
     err_T = np.zeros(K)
     err_if = np.zeros(K)
     traces = np.zeros((max(2 * (n_sub - 1), 1), g.nt, g.nx)) if want_traces else None
-    rc = _load().orc_swr_pq(b.ref(), KIND[kind], p, p if q is None else q, overlap, n_sub, K, _ptr(uT_sub),
-                            _ptr(uT), _ptr(UT), _ptr(err_T), _ptr(err_if), _ptr(traces))
+    fn = {"jacobi": _load().orc_swr_pq, "gauss_seidel": _load().orc_swr_gs}[schedule]
+    rc = fn(b.ref(), KIND[kind], p, p if q is None else q, overlap, n_sub, K, _ptr(uT_sub),
+            _ptr(uT), _ptr(UT), _ptr(err_T), _ptr(err_if), _ptr(traces))
     if rc != 0:
         raise ValueError("orc_swr rejected the arguments")
     slabs, off = [], 0

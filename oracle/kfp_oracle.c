@@ -309,8 +309,8 @@ int orc_window(const orc_problem *P, int lo, int hi, int ltype, int rtype, doubl
  *                (between s=i and s=i+1) first toLeft[i] (sent by i+1, used at hi_i)
  *                then toRight[i] (sent by i, used at lo_{i+1}); may be NULL.
  */
-int orc_swr_pq(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K,
-               double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
+static int swr_impl(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K, int gauss_seidel,
+                    double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
     const int nx = P->nx, nt = P->nt, nv = P->nv, S = n_sub;
     if (S < 1 || nv % S != 0 || K < 1) return -1;
     int32_t *lo = (int32_t *)malloc(sizeof(int32_t) * S), *hi = (int32_t *)malloc(sizeof(int32_t) * S);
@@ -345,7 +345,9 @@ int orc_swr_pq(const orc_problem *P, int kind, double p, double q, int overlap, 
         size_t off = 0;
         for (int s = 0; s < S; ++s) {
             int lt = (s == 0) ? END_PHYS : etype, rt = (s == S - 1) ? END_PHYS : etype;
-            const double *gL = (s > 0) ? toR_in + (size_t)(s - 1) * TR : NULL;
+            /* Jacobi: both incoming traces from iteration k-1.  Gauss-Seidel (SWR1-SWR4,
+             * P:554-585, in subdomain order): the left trace is the one s-1 sent in this iteration. */
+            const double *gL = (s > 0) ? (gauss_seidel ? toR_out : toR_in) + (size_t)(s - 1) * TR : NULL;
             const double *gR = (s < S - 1) ? toL_in + (size_t)s * TR : NULL;
             int sendL = (s > 0) ? hi[s - 1] : -1, sendR = (s < S - 1) ? lo[s + 1] : -1;
             int nrec = 0, rn[2];
@@ -397,6 +399,15 @@ int orc_swr_pq(const orc_problem *P, int kind, double p, double q, int overlap, 
     free(lo); free(hi); free(lines); free(Ulines); free(Ut);
     free(toL_in); free(toR_in); free(toL_out); free(toR_out); free(slabs); free(rec);
     return 0;
+}
+int orc_swr_pq(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K,
+               double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
+    return swr_impl(P, kind, p, q, overlap, n_sub, K, 0, uT_sub, uT, UT, err_T, err_if, traces);
+}
+/* Gauss-Seidel schedule (the paper's serial SWR1-SWR4, subdomains in increasing v). */
+int orc_swr_gs(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K,
+               double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
+    return swr_impl(P, kind, p, q, overlap, n_sub, K, 1, uT_sub, uT, UT, err_T, err_if, traces);
 }
 int orc_swr(const orc_problem *P, int kind, double p, int overlap, int n_sub, int K,
             double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {

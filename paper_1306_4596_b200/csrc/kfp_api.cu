@@ -319,6 +319,7 @@ struct kfp_problem_s {
     bool setup = false;
     int kind = 0;
     double p = 0, q_rob = 0;  // Robin parameters: p on right (hi) ends, q_rob on left (lo) ends
+    bool gauss_seidel = false;  // schedule: Jacobi (false) or Gauss-Seidel SWR1-SWR4 (true)
     int ov = 0, S = 0, s_begin = 0, s_end = 0, K_max = 0, k_done = 0;
     std::vector<int> lo, hi;
     std::vector<SubDev> subs;  // local block
@@ -1220,6 +1221,7 @@ kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
         warn = "warning: Dirichlet transmission without overlap does not converge (P:661)";
 
     pb->kind = kind;
+    pb->gauss_seidel = false;
     pb->p = p;
     pb->q_rob = (kind == KFP_ROBIN) ? q : p;
     pb->ov = overlap;
@@ -1397,6 +1399,23 @@ kfp_status kfp_swr_reset(kfp_problem pb) {
     return KFP_OK;
 }
 
+kfp_status kfp_swr_set_schedule(kfp_problem pb, kfp_schedule schedule) {
+    if (!pb || !pb->setup) {
+        set_err("kfp_swr_set_schedule: no setup");
+        return KFP_E_STATE;
+    }
+    if (schedule != KFP_JACOBI && schedule != KFP_GAUSS_SEIDEL) {
+        set_err("kfp_swr_set_schedule: unknown schedule %d", (int)schedule);
+        return KFP_E_INVAL;
+    }
+    if (schedule == KFP_GAUSS_SEIDEL && (pb->s_begin != 0 || pb->s_end != pb->S || pb->plan.window)) {
+        set_err("kfp_swr_set_schedule: Gauss-Seidel needs every subdomain on this process and a per-step plan");
+        return KFP_E_INVAL;
+    }
+    pb->gauss_seidel = (schedule == KFP_GAUSS_SEIDEL);
+    return KFP_OK;
+}
+
 kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
     if (!pb || !pb->setup) {
         set_err("kfp_swr_iterate: no setup");
@@ -1430,10 +1449,27 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
         const int k = pb->k_done + 1;  // 1-based iteration number
         P.par_in = (k - 1) & 1;
         P.par_out = k & 1;
+        P.par_in_lo = pb->gauss_seidel ? P.par_out : P.par_in;
         P.errT = pb->d_errT + (k - 1);
         P.errIF = pb->d_errIF + (k - 1);
         KFP_CUDA(cudaEventRecord(pb->ev[2 + 2 * it], pb->stream));
-        if (pb->plan.window) {
+        if (pb->gauss_seidel) {
+            // SWR1-SWR4: the subdomains in increasing v, each over the whole window, each
+            // reading the trace its left neighbour wrote in this iteration (stream order)
+            const Plan &pl = pb->plan;
+            for (int s = 0; s < nloc; ++s) {
+                StepParams Ps = P;
+                Ps.subs = pb->d_subs + s;
+                FusedData fs = pb->fd;  // the tables of subdomain s
+                if (fs.maps) fs.maps += 2 * s;
+                if (fs.l2c) fs.l2c += (size_t)s * pl.C * kfp::kL2M;
+                if (fs.ctab) fs.ctab += (size_t)s * 4 * pl.P * kfp::kCT;
+                for (int n = 0; n < pb->nt; ++n) {
+                    Ps.last = (n + 1 == pb->nt);
+                    if (kfp_status st = launch_step(pb, pl, Ps, 1, n, fs)) return st;
+                }
+            }
+        } else if (pb->plan.window) {
             if (kfp_status st = launch_window(pb, pb->plan, P, nloc, pb->fd, 0, pb->nt)) return st;
         } else {
             for (int n = 0; n < pb->nt; ++n) {
@@ -1619,6 +1655,7 @@ extern "C" int kfp_debug_trace_step(kfp_problem pb, int n, unsigned long long *h
     P.errIF = pb->d_errIF;
     P.par_in = 0;
     P.par_out = 1;
+    P.par_in_lo = 0;
     P.last = 0;
     launch_step(pb, pb->plan, P, (int)pb->subs.size(), n, pb->fd);
     cudaDeviceSynchronize();

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(P_ * kWarp, (P_ >= 16) ? 1 : 16 / P_) step_col
             const int qq = lane >> 3, mc = m0 + (lane & (kColW - 1));
             const size_t go = static_cast<size_t>(P.n) * P.nx + mc;
             double v = 0.0;
-            if (qq == 0 && S.ltype != END_PHYS) v = __ldg(S.gL[P.par_in] + go);
+            if (qq == 0 && S.ltype != END_PHYS) v = __ldg(S.gL[P.par_in_lo] + go);
             if (qq == 1 && S.rtype != END_PHYS) v = __ldg(S.gR[P.par_in] + go);
             if (qq == 2 && S.ifL >= 0 && P.Ulines) v = __ldg(P.Ulines + (static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + mc);
             if (qq == 3 && S.ifR >= 0 && P.Ulines) v = __ldg(P.Ulines + (static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + mc);

@@ -64,6 +64,8 @@ struct StepParams {
     int nx, nv, nt;
     int n;                 // this launch computes level n+1
     int par_in, par_out;   // iteration parities of the traces read / written
+    int par_in_lo;         // parity of the incoming LEFT trace: par_in (Jacobi) or par_out
+                           // (Gauss-Seidel SWR1-SWR4: the left neighbour already ran this iteration)
     int from_u0;           // n == 0: u^0 from the u0 tables (no slab read)
     int last;              // n+1 == nt
     int send_robin;        // outgoing trace kind: 0 Dirichlet value, 1 Robin combination
@@ -279,7 +281,7 @@ __device__ __forceinline__ void pass_a(const StepParams &P, const Tile &t, doubl
         if (i == S.iL_tr) rtr[lane] = rr;
         if (i == S.iR_tr) rtr[kWarp + lane] = rr;
         if (i == 0 && S.ltype != END_PHYS) {
-            const double g = S.gL[P.par_in][static_cast<size_t>(P.n) * P.nx + t.m];
+            const double g = S.gL[P.par_in_lo][static_cast<size_t>(P.n) * P.nx + t.m];
             rr = fma(S.injL, g, rr);
             if (S.ltype == END_DIRI && S.iL_tr == -1 && active)  // Dirichlet, no overlap: the end node is the trace node
                 S.sendL[P.par_out][static_cast<size_t>(P.n) * P.nx + t.m] = g;

@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
 #pragma unroll
         for (int r = 0; r < NR; ++r) fx[r] = (r < P.f_rank) ? P.cf[r] * __ldg(P.fx + r * P.nx + m) : 0.0;
         if (warp == 0) {  // incoming traces of this step (written by the previous iteration)
-            sm.gin[lane] = (S.ltype != END_PHYS) ? S.gL[P.par_in][goff] : 0.0;
+            sm.gin[lane] = (S.ltype != END_PHYS) ? S.gL[P.par_in_lo][goff] : 0.0;
             sm.gin[kWarp + lane] = (S.rtype != END_PHYS) ? S.gR[P.par_in][goff] : 0.0;
         }
 

@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 1) step_window(const WinParams W) 
         for (int r = 0; r < NR; ++r)
             fx[r] = (r < P.f_rank) ? __ldg(W.cfn + static_cast<size_t>(n) * kMaxRank + r) * __ldg(P.fx + r * P.nx + m) : 0.0;
         if (warp == 0) {  // incoming traces of this step (written by the previous iteration)
-            sm.gin[j & 1][lane] = (S.ltype != END_PHYS) ? __ldg(S.gL[P.par_in] + goff) : 0.0;
+            sm.gin[j & 1][lane] = (S.ltype != END_PHYS) ? __ldg(S.gL[P.par_in_lo] + goff) : 0.0;
             sm.gin[j & 1][kWarp + lane] = (S.rtype != END_PHYS) ? __ldg(S.gR[P.par_in] + goff) : 0.0;
         }
         double hend = 0.0, kst = 0.0;

@@ -20,7 +20,7 @@ KIND = {"dirichlet": 0, "robin": 1}
 
 # Every symbol include/kfp.h declares (checked by tests/test_abi.py).
 SYMBOLS = (
-    "kfp_problem_create", "kfp_problem_destroy", "kfp_set_stream", "kfp_monodomain_solve", "kfp_swr_setup", "kfp_swr_setup_pq", "kfp_swr_solve_pq",
+    "kfp_problem_create", "kfp_problem_destroy", "kfp_set_stream", "kfp_monodomain_solve", "kfp_swr_setup", "kfp_swr_setup_pq", "kfp_swr_solve_pq", "kfp_swr_set_schedule",
     "kfp_swr_reset", "kfp_swr_iterate", "kfp_swr_edge_buffers", "kfp_swr_bind_edge_buffers", "kfp_swr_solve", "kfp_error_history",
     "kfp_swr_subdomain_uT", "kfp_swr_subdomain_range", "kfp_swr_trace", "kfp_monodomain_uT", "kfp_launch_count",
     "kfp_plan", "kfp_last_timing", "kfp_last_error",
@@ -67,6 +67,7 @@ def load(path: str = LIB_PATH):
         "kfp_monodomain_solve": (i32, [vp, vp]),
         "kfp_swr_setup": (i32, [vp, i32, dbl, i32, i32, i32, i32, i32]),
         "kfp_swr_setup_pq": (i32, [vp, i32, dbl, dbl, i32, i32, i32, i32, i32]),
+        "kfp_swr_set_schedule": (i32, [vp, i32]),
         "kfp_swr_solve_pq": (i32, [vp, i32, dbl, dbl, i32, i32, i32, vp]),
         "kfp_swr_reset": (i32, [vp]),
         "kfp_swr_iterate": (i32, [vp, i32]),
@@ -164,6 +165,10 @@ class Problem:
             _check(load().kfp_swr_setup_pq(self._h, KIND[kind], float(p), float(q), int(overlap), int(n_sub),
                                            int(s_begin), int(s_end), int(K_max)))
         self.n_sub, self.s_begin, self.s_end = n_sub, s_begin, s_end
+
+    def set_schedule(self, schedule: str):
+        """'jacobi' (default after setup) or 'gauss_seidel' (the paper's SWR1-SWR4, single process)."""
+        _check(load().kfp_swr_set_schedule(self._h, {"jacobi": 0, "gauss_seidel": 1}[schedule]))
 
     def reset(self):
         _check(load().kfp_swr_reset(self._h))

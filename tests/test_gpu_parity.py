@@ -255,3 +255,44 @@ def test_alternative_kernels_c2_full_size(kfp, monkeypatch, alt):
         assert rel(g["uT_sub"][s], realize(m["c_sub"][s], run.grid.nx)) <= TOL, (alt, s)
     assert rel(g["err_T"], m["err_T"]) <= TOL
     assert rel(g["err_if"], m["err_if"]) <= TOL
+
+
+GS_CASES = ["c0", "c1", "robin_ov3", "oswr_pq_ov_S4", "c4_small", "chunk33_robin", "ragged_dirichlet_ov"]
+
+
+@functools.lru_cache(maxsize=None)
+def _oracle_gs(run):
+    import oracle
+
+    return oracle.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q,
+                      schedule="gauss_seidel")
+
+
+@pytest.mark.parametrize("alt", ["default", "column"])
+@pytest.mark.parametrize("name", GS_CASES)
+def test_gauss_seidel_vs_oracle(kfp, monkeypatch, alt, name):
+    """The paper's serial SWR1-SWR4 schedule on the GPU: per-subdomain launch sequences in
+    increasing v, each reading its left neighbour's trace of the same iteration."""
+    if alt == "column":
+        monkeypatch.setenv("KFP_COL", "1")
+    run = CASES[name]
+    with kfp.Problem(ki.make_problem(run)) as pb:
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
+        pb.set_schedule("gauss_seidel")
+        pb.reset()
+        pb.iterate(run.K)
+        eT, eI = pb.history()
+        slabs = [pb.subdomain_uT(s) for s in range(run.n_sub)]
+    r = _oracle_gs(run)
+    for s, (a, b) in enumerate(zip(slabs, r["uT_sub"])):
+        assert rel(a, b) <= TOL, (name, s)
+    assert rel(eT, r["err_T"]) <= TOL and rel(eI, r["err_if"]) <= TOL
+
+
+def test_gauss_seidel_rejected_by_window_plan(kfp, monkeypatch):
+    monkeypatch.setenv("KFP_WINDOW", "1")
+    run = CASES["c0"]
+    with kfp.Problem(ki.make_problem(run)) as pb:
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        with pytest.raises(kfp.KfpError):
+            pb.set_schedule("gauss_seidel")

@@ -312,3 +312,29 @@ def test_two_sided_beats_one_sided(orc):
     two = {(p, q): orc.swr(prob, "robin", p, 0, 2, run.K, q=q)["err_if"][-1] for p in ps for q in ps}
     assert all(two[(p, p)] == one[p] for p in ps)
     assert min(two.values()) < 0.7 * min(one.values()), (min(one.values()), min(two.values()))
+
+
+@pytest.mark.parametrize("kind,p,ov", [("robin", 2.0, 0), ("dirichlet", 0.0, 4)])
+def test_gauss_seidel_is_interleaved_jacobi(orc, kind, p, ov):
+    """The paper's serial SWR1-SWR4 against its parallel Remark: for two
+    subdomains from zero traces, Gauss-Seidel iterate k of subdomain 0 is Jacobi iterate 2k-1 and
+    of subdomain 1 Jacobi iterate 2k -- the Jacobi sequence interleaves two Gauss-Seidel sequences.
+    Same arithmetic on both sides, so the identity is bitwise."""
+    run = ki.scaled(ki.config("c0"), nt=30, K=5)
+    prob = ki.make_problem(run)
+    K = 5
+    gs = orc.swr(prob, kind, p, ov, 2, K, schedule="gauss_seidel")
+    assert np.array_equal(gs["uT_sub"][0], orc.swr(prob, kind, p, ov, 2, 2 * K - 1)["uT_sub"][0])
+    assert np.array_equal(gs["uT_sub"][1], orc.swr(prob, kind, p, ov, 2, 2 * K)["uT_sub"][1])
+
+
+def test_gauss_seidel_converges_to_monodomain(orc):
+    """Gauss-Seidel has the same fixed point (the monodomain solution) and, per iteration,
+    converges at least as fast as Jacobi on a 4-subdomain Robin problem (err_if at every k >= 5)."""
+    run = ki.scaled(ki.config("c1"), nx=32, nv=64, nt=100, K=30)
+    prob = ki.make_problem(run)
+    gs = orc.swr(prob, "robin", 4.0, 0, 4, 30, schedule="gauss_seidel")
+    ja = orc.swr(prob, "robin", 4.0, 0, 4, 30)
+    assert np.all(gs["err_if"][4:] <= ja["err_if"][4:] * (1 + 1e-12))
+    gs = orc.swr(prob, "robin", 4.0, 0, 4, 160, schedule="gauss_seidel")
+    assert gs["err_T"][-1] < 1e-11 * np.abs(gs["UT"]).max(), gs["err_T"][-1]
