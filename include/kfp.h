@@ -168,6 +168,22 @@ kfp_status kfp_swr_bind_edge_buffers(kfp_problem pb, int32_t parity, double *sen
 kfp_status kfp_swr_solve(kfp_problem pb, kfp_kind kind, double p, int32_t overlap, int32_t n_sub, int32_t K,
                          double *uT);
 
+/* Batched Robin-parameter sweep (the Fig. 1 experiment): n_rep
+ * independent replicas of the decomposition, replica r solved with OSWR(ps[r], qs[r]) (qs = NULL: one-sided
+ * qs = ps; ignored for KFP_DIRICHLET), all in the same launches.  Single process; the other arguments as
+ * kfp_swr_setup.  Then kfp_swr_reset / kfp_swr_iterate / kfp_swr_set_schedule as usual;
+ * kfp_error_history and kfp_swr_subdomain_uT report replica 0, the _batch_ calls any replica.
+ * ps, qs: host arrays of n_rep doubles, copied. */
+kfp_status kfp_swr_setup_batch(kfp_problem pb, kfp_kind kind, const double *ps, const double *qs, int32_t n_rep,
+                               int32_t overlap, int32_t n_sub, int32_t K_max);
+
+/* Error history (as kfp_error_history) of replica rep of a batch. */
+kfp_status kfp_swr_batch_history(kfp_problem pb, int32_t rep, int32_t cap, int32_t *K_out, double *err_T,
+                                 double *err_if);
+
+/* u^k(T) of subdomain s (0 <= s < n_sub) of replica rep, host [(hi_s - lo_s + 1) * nx]. */
+kfp_status kfp_swr_batch_subdomain_uT(kfp_problem pb, int32_t rep, int32_t s, double *out);
+
 /* kfp_swr_solve with OSWR(p, q) (see kfp_swr_setup_pq). */
 kfp_status kfp_swr_solve_pq(kfp_problem pb, kfp_kind kind, double p, double q, int32_t overlap, int32_t n_sub,
                             int32_t K, double *uT);

@@ -139,14 +139,15 @@ bool col_kernel(int B, int NR, int P, ColKernel *k, size_t *smem) {
 // Fused path: P = 16 warps per CTA, chunks of L rows (target 17), row blocks of
 // R = 16 L rows, C = ceil(n_max / R) <= 8 CTAs per cluster.  Otherwise the
 // three-phase path (P = 8, b = 32, block aggregates through global memory).
-Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool allow_window = false, int nx = 0) {
+Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool allow_window = false, int nx = 0,
+               bool allow_col = true) {
     Plan pl;
     const int n_max = *std::max_element(ns.begin(), ns.end());
     const int NR = (f_rank <= 2) ? 2 : 4;
     // Column-tile kernel (opt-in, KFP_COL=1; correct, but measured slower than the cluster kernel on c2
     // and c4): 8-column tiles, the whole column in one CTA of P = 8 (2 CTAs per SM,
     // n <= 1056) or 16 warps (n <= 2112), chunks of L <= 33 rows.
-    if (allow_fused && nx > 0 && nx % kfp::kColW == 0 && NR == 2 && getenv("KFP_COL") && !getenv("KFP_WINDOW") &&
+    if (allow_col && allow_fused && nx > 0 && nx % kfp::kColW == 0 && NR == 2 && getenv("KFP_COL") && !getenv("KFP_WINDOW") &&
         n_max <= 4 * 16 * 33 && (int)ns.size() <= kfp::kColMaxSub) {
         const int P = (n_max <= 4 * 8 * 33) ? 8 : 16;
         int L = (n_max + 4 * P - 1) / (4 * P);
@@ -320,6 +321,7 @@ struct kfp_problem_s {
     int kind = 0;
     double p = 0, q_rob = 0;  // Robin parameters: p on right (hi) ends, q_rob on left (lo) ends
     bool gauss_seidel = false;  // schedule: Jacobi (false) or Gauss-Seidel SWR1-SWR4 (true)
+    int n_rep = 1;              // independent replicas of the decomposition (batched Robin-parameter sweep)
     int ov = 0, S = 0, s_begin = 0, s_end = 0, K_max = 0, k_done = 0;
     std::vector<int> lo, hi;
     std::vector<SubDev> subs;  // local block
@@ -1182,8 +1184,14 @@ kfp_status kfp_swr_setup(kfp_problem pb, kfp_kind kind, double p, int32_t overla
     return kfp_swr_setup_pq(pb, kind, p, p, overlap, n_sub, s_begin, s_end, K_max);
 }
 
-kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, int32_t overlap, int32_t n_sub,
-                            int32_t s_begin, int32_t s_end, int32_t K_max) {
+}  // extern "C"
+
+namespace {
+// Setup of n_rep independent replicas of the decomposition (replica r: OSWR(ps[r], qs[r])); n_rep = 1 is
+// the ordinary solve (kfp_swr_setup_pq), n_rep > 1 the batched parameter sweep (kfp_swr_setup_batch).
+kfp_status swr_setup_impl(kfp_problem pb, kfp_kind kind, const double *ps, const double *qs, int n_rep,
+                          int32_t overlap, int32_t n_sub, int32_t s_begin, int32_t s_end, int32_t K_max) {
+    const double p = ps[0], q = qs[0];
     if (!pb) {
         set_err("kfp_swr_setup: NULL problem");
         return KFP_E_INVAL;
@@ -1192,10 +1200,13 @@ kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
         set_err("kfp_swr_setup: unknown kind %d", (int)kind);
         return KFP_E_INVAL;
     }
-    if (kind == KFP_ROBIN && !(p > 0 && q > 0)) {
-        set_err("kfp_swr_setup: Robin parameters p, q must be > 0 (P:58), got %g, %g", p, q);
-        return KFP_E_INVAL;
-    }
+    for (int r = 0; r < n_rep; ++r)
+        if (kind == KFP_ROBIN && !(ps[r] > 0 && qs[r] > 0)) {
+            set_err("kfp_swr_setup: Robin parameters p, q must be > 0 (P:58), got %g, %g", ps[r], qs[r]);
+            return KFP_E_INVAL;
+        }
+    (void)p;
+    (void)q;
     if (n_sub < 1 || pb->nv % n_sub != 0) {
         set_err("kfp_swr_setup: n_sub=%d must divide nv=%d", n_sub, pb->nv);
         return KFP_E_INVAL;
@@ -1213,6 +1224,10 @@ kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
         set_err("kfp_swr_setup: K_max must be >= 1 (SPEC S:214)");
         return KFP_E_INVAL;
     }
+    if (n_rep < 1 || (n_rep > 1 && (s_begin != 0 || s_end != n_sub))) {
+        set_err("kfp_swr_setup: a batch of %d replicas needs every subdomain on this process", n_rep);
+        return KFP_E_INVAL;
+    }
     KFP_CUDA(cudaSetDevice(pb->device));
     KFP_CUDA(cudaStreamSynchronize(pb->stream));
     free_swr(pb);
@@ -1222,8 +1237,9 @@ kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
 
     pb->kind = kind;
     pb->gauss_seidel = false;
-    pb->p = p;
-    pb->q_rob = (kind == KFP_ROBIN) ? q : p;
+    pb->n_rep = n_rep;
+    pb->p = ps[0];
+    pb->q_rob = (kind == KFP_ROBIN) ? qs[0] : ps[0];
     pb->ov = overlap;
     pb->S = n_sub;
     pb->s_begin = s_begin;
@@ -1259,10 +1275,11 @@ kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
     const int nloc = s_end - s_begin;
     const size_t nx = pb->nx, TR = (size_t)pb->nt * nx;
     int n_max = 0;
-    pb->subs.resize(nloc);
-    for (int i = 0; i < nloc; ++i) {
-        const int s = s_begin + i;
-        SubDev &sd = pb->subs[i];
+    const int ntot = n_rep * nloc;  // all subdomains of all replicas (replica-major)
+    pb->subs.resize(ntot);
+    for (int ii = 0; ii < ntot; ++ii) {
+        const int rr = ii / nloc, i = ii - rr * nloc, s = s_begin + i;
+        SubDev &sd = pb->subs[ii];
         std::memset(&sd, 0, sizeof sd);
         sd.lo = pb->lo[s];
         sd.hi = pb->hi[s];
@@ -1283,16 +1300,20 @@ kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
             set_err("kfp_swr_setup: subdomain %d has %d unknown rows (need >= 2)", s, sd.n);
             return KFP_E_INVAL;
         }
-        woodbury(pb, sd, pb->q_rob, p);
+        sd.grp = rr;
+        sd.tpL = ps[rr];                                   // sent left: lands on a right end (p)
+        sd.tpR = (kind == KFP_ROBIN) ? qs[rr] : ps[rr];    // sent right: lands on a left end (q)
+        woodbury(pb, sd, (kind == KFP_ROBIN) ? qs[rr] : ps[rr], ps[rr]);
         n_max = std::max(n_max, sd.n);
     }
     std::vector<int> ns;
     for (const SubDev &sd : pb->subs) ns.push_back(sd.n);
-    pb->plan = make_plan(ns, pb->f_rank, true, true, pb->nx);
+    pb->plan = make_plan(ns, pb->f_rank, true, n_rep == 1, pb->nx, n_rep == 1);
     Plan &pl = pb->plan;
     // the rows of each outgoing trace stencil must sit in one row block
-    for (int i = 0; i < nloc; ++i) {
-        SubDev &sd = pb->subs[i];
+    for (int ii = 0; ii < ntot; ++ii) {
+        const int i = ii % nloc;
+        SubDev &sd = pb->subs[ii];
         sd.nblk = (sd.n + pl.R - 1) / pl.R;
         auto same = [&](int r1, int r2) { return r1 / pl.R == r2 / pl.R; };
         const bool rob = (kind == KFP_ROBIN);
@@ -1310,33 +1331,35 @@ kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
     if (kfp_status st = ensure_qtab(pb, std::max(pl.R, n_max) + 2)) return st;
     if (kfp_status st = configure_kernels(pl)) return st;
 
-    // slabs and traces
-    std::vector<double *> toL(2 * std::max(0, nloc - 1)), toR(2 * std::max(0, nloc - 1));
-    for (int i = 0; i < nloc; ++i) {
-        SubDev &sd = pb->subs[i];
+    // slabs and traces (each replica its own chain of interfaces)
+    for (int ii = 0; ii < ntot; ++ii) {
+        SubDev &sd = pb->subs[ii];
         const size_t rows = (size_t)(sd.hi - sd.lo + 1);
         for (int q = 0; q < 2; ++q)
             if (kfp_status st = swr_alloc(pb, &sd.slab[q], rows * nx)) return st;
     }
-    for (int i = 0; i + 1 < nloc; ++i)
-        for (int q = 0; q < 2; ++q) {
-            if (kfp_status st = swr_alloc(pb, &toL[2 * i + q], TR)) return st;
-            if (kfp_status st = swr_alloc(pb, &toR[2 * i + q], TR)) return st;
-            if (q == 0) {
-                pb->zero_on_reset.push_back(toL[2 * i]);
-                pb->zero_on_reset.push_back(toR[2 * i]);
+    for (int rr = 0; rr < n_rep; ++rr) {
+        std::vector<double *> toL(2 * std::max(0, nloc - 1)), toR(2 * std::max(0, nloc - 1));
+        for (int i = 0; i + 1 < nloc; ++i)
+            for (int q = 0; q < 2; ++q) {
+                if (kfp_status st = swr_alloc(pb, &toL[2 * i + q], TR)) return st;
+                if (kfp_status st = swr_alloc(pb, &toR[2 * i + q], TR)) return st;
+                if (q == 0) {
+                    pb->zero_on_reset.push_back(toL[2 * i]);
+                    pb->zero_on_reset.push_back(toR[2 * i]);
+                }
             }
-        }
-    for (int i = 0; i < nloc; ++i) {
-        SubDev &sd = pb->subs[i];
-        for (int q = 0; q < 2; ++q) {
-            if (i + 1 < nloc) {
-                sd.gR[q] = toL[2 * i + q];
-                sd.sendR[q] = toR[2 * i + q];
-            }
-            if (i > 0) {
-                sd.gL[q] = toR[2 * (i - 1) + q];
-                sd.sendL[q] = toL[2 * (i - 1) + q];
+        for (int i = 0; i < nloc; ++i) {
+            SubDev &sd = pb->subs[rr * nloc + i];
+            for (int q = 0; q < 2; ++q) {
+                if (i + 1 < nloc) {
+                    sd.gR[q] = toL[2 * i + q];
+                    sd.sendR[q] = toR[2 * i + q];
+                }
+                if (i > 0) {
+                    sd.gL[q] = toR[2 * (i - 1) + q];
+                    sd.sendL[q] = toL[2 * (i - 1) + q];
+                }
             }
         }
     }
@@ -1357,29 +1380,79 @@ kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
         }
     {
         void *q = nullptr;
-        KFP_CUDA(cudaMalloc(&q, sizeof(SubDev) * nloc));
+        KFP_CUDA(cudaMalloc(&q, sizeof(SubDev) * ntot));
         pb->d_subs = static_cast<SubDev *>(q);
-        KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max));
+        KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max * n_rep));
         pb->d_errT = static_cast<unsigned long long *>(q);
-        KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max));
+        KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max * n_rep));
         pb->d_errIF = static_cast<unsigned long long *>(q);
     }
-    KFP_CUDA(cudaMemcpy(pb->d_subs, pb->subs.data(), sizeof(SubDev) * nloc, cudaMemcpyHostToDevice));
+    KFP_CUDA(cudaMemcpy(pb->d_subs, pb->subs.data(), sizeof(SubDev) * ntot, cudaMemcpyHostToDevice));
     {
         std::vector<void *> own;
         kfp_status st = build_tmaps(pb, pl, pb->subs, &pb->fd.maps, &own);
         if (!st) st = build_l2m(pb, pl, pb->subs, &pb->fd.l2c, &own);
         if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &pb->fd.coefT, &pb->fd.tabs, &own);
-        if (!st) st = build_window_tables(pb, pl, nloc, &pb->fd, &own);
+        if (!st) st = build_window_tables(pb, pl, ntot, &pb->fd, &own);
         if (!st) st = build_col_tables(pb, pl, pb->subs, &pb->fd, &own);
         for (void *q : own) pb->swr_allocs.push_back(static_cast<double *>(q));
         if (st) return st;
     }
-    if (kfp_status st = alloc_general_scratch(pb, pl, nloc, &pb->d_blkagg, &pb->d_chkagg, &pb->d_carry, pb->swr_allocs))
+    if (kfp_status st = alloc_general_scratch(pb, pl, ntot, &pb->d_blkagg, &pb->d_chkagg, &pb->d_carry, pb->swr_allocs))
         return st;
     pb->setup = true;
     if (kfp_status st = kfp_swr_reset(pb)) return st;
     g_err = warn;
+    return KFP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+kfp_status kfp_swr_setup_pq(kfp_problem pb, kfp_kind kind, double p, double q, int32_t overlap, int32_t n_sub,
+                            int32_t s_begin, int32_t s_end, int32_t K_max) {
+    return swr_setup_impl(pb, kind, &p, &q, 1, overlap, n_sub, s_begin, s_end, K_max);
+}
+
+kfp_status kfp_swr_setup_batch(kfp_problem pb, kfp_kind kind, const double *ps, const double *qs, int32_t n_rep,
+                               int32_t overlap, int32_t n_sub, int32_t K_max) {
+    if (!ps || n_rep < 1) {
+        set_err("kfp_swr_setup_batch: need n_rep >= 1 parameters");
+        return KFP_E_INVAL;
+    }
+    return swr_setup_impl(pb, kind, ps, qs ? qs : ps, n_rep, overlap, n_sub, 0, n_sub, K_max);
+}
+
+kfp_status kfp_swr_batch_history(kfp_problem pb, int32_t rep, int32_t cap, int32_t *K_out, double *err_T,
+                                 double *err_if) {
+    if (!pb || !pb->setup || rep < 0 || rep >= pb->n_rep || pb->k_done == 0 || cap < pb->k_done) {
+        set_err("kfp_swr_batch_history: bad replica, no iteration or cap < K");
+        return pb && pb->setup && pb->k_done == 0 ? KFP_E_STATE : KFP_E_INVAL;
+    }
+    std::vector<unsigned long long> a(pb->k_done), b(pb->k_done);
+    const size_t off = (size_t)rep * pb->K_max;
+    KFP_CUDA(cudaMemcpyAsync(a.data(), pb->d_errT + off, sizeof(unsigned long long) * pb->k_done, cudaMemcpyDeviceToHost,
+                             pb->stream));
+    KFP_CUDA(cudaMemcpyAsync(b.data(), pb->d_errIF + off, sizeof(unsigned long long) * pb->k_done,
+                             cudaMemcpyDeviceToHost, pb->stream));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    for (int k = 0; k < pb->k_done; ++k) {
+        std::memcpy(&err_T[k], &a[k], 8);
+        std::memcpy(&err_if[k], &b[k], 8);
+    }
+    *K_out = pb->k_done;
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_batch_subdomain_uT(kfp_problem pb, int32_t rep, int32_t s, double *out) {
+    if (!pb || !pb->setup || rep < 0 || rep >= pb->n_rep || s < 0 || s >= pb->S || pb->k_done == 0 || !out) {
+        set_err("kfp_swr_batch_subdomain_uT: bad replica/subdomain or no iteration");
+        return KFP_E_INVAL;
+    }
+    const SubDev &sd = pb->subs[(size_t)rep * pb->S + s];
+    KFP_CUDA(cudaMemcpyAsync(out, sd.slab[pb->nt & 1], sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
+                             cudaMemcpyDeviceToHost, pb->stream));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
     return KFP_OK;
 }
 
@@ -1393,8 +1466,8 @@ kfp_status kfp_swr_reset(kfp_problem pb) {
     for (double *p : pb->zero_on_reset) KFP_CUDA(cudaMemsetAsync(p, 0, TR * sizeof(double), pb->stream));
     if (pb->edge_recvL[0]) KFP_CUDA(cudaMemsetAsync(pb->edge_recvL[0], 0, TR * sizeof(double), pb->stream));
     if (pb->edge_recvR[0]) KFP_CUDA(cudaMemsetAsync(pb->edge_recvR[0], 0, TR * sizeof(double), pb->stream));
-    KFP_CUDA(cudaMemsetAsync(pb->d_errT, 0, sizeof(unsigned long long) * pb->K_max, pb->stream));
-    KFP_CUDA(cudaMemsetAsync(pb->d_errIF, 0, sizeof(unsigned long long) * pb->K_max, pb->stream));
+    KFP_CUDA(cudaMemsetAsync(pb->d_errT, 0, sizeof(unsigned long long) * pb->K_max * pb->n_rep, pb->stream));
+    KFP_CUDA(cudaMemsetAsync(pb->d_errIF, 0, sizeof(unsigned long long) * pb->K_max * pb->n_rep, pb->stream));
     pb->k_done = 0;
     return KFP_OK;
 }
@@ -1438,7 +1511,6 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
     P.subs = pb->d_subs;
     P.send_robin = (pb->kind == KFP_ROBIN);
     P.p = pb->p;
-    P.q_lo = pb->q_rob;
     P.UT = pb->d_UT;
     P.Ulines = pb->d_Ulines;
     P.blkagg = pb->d_blkagg;
@@ -1452,6 +1524,7 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
         P.par_in_lo = pb->gauss_seidel ? P.par_out : P.par_in;
         P.errT = pb->d_errT + (k - 1);
         P.errIF = pb->d_errIF + (k - 1);
+        P.err_stride = pb->K_max;  // replica r's slots: + r * K_max
         KFP_CUDA(cudaEventRecord(pb->ev[2 + 2 * it], pb->stream));
         if (pb->gauss_seidel) {
             // SWR1-SWR4: the subdomains in increasing v, each over the whole window, each
@@ -1648,11 +1721,11 @@ extern "C" int kfp_debug_trace_step(kfp_problem pb, int n, unsigned long long *h
     P.subs = pb->d_subs;
     P.send_robin = (pb->kind == KFP_ROBIN);
     P.p = pb->p;
-    P.q_lo = pb->q_rob;
     P.UT = pb->d_UT;
     P.Ulines = pb->d_Ulines;
     P.errT = pb->d_errT;
     P.errIF = pb->d_errIF;
+    P.err_stride = pb->K_max;
     P.par_in = 0;
     P.par_out = 1;
     P.par_in_lo = 0;

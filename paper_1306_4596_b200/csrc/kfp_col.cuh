@@ -451,11 +451,11 @@ __global__ void __launch_bounds__(P_ * kWarp, (P_ >= 16) ? 1 : 16 / P_) step_col
             const double xe1 = x_at(n - 1, &sm.kb[3 * kColW + cc], Yf, Xf);
             if (lane == 0) {
                 if (S.iL_tr >= 0)  // (p + d_v) u at hi_{s-1}, half-cell flux on [c, c+h/2]
-                    S.sendL[P.par_out][go] = rob ? P.p * xL - ((xL - xL1) * inv_h + half_h_dt * (xL - sm.rtr[0 * kColW + cc])) : xL;
+                    S.sendL[P.par_out][go] = rob ? S.tpL * xL - ((xL - xL1) * inv_h + half_h_dt * (xL - sm.rtr[0 * kColW + cc])) : xL;
                 else if (S.iL_tr == -1)
                     S.sendL[P.par_out][go] = gl;  // Dirichlet without overlap: the end node is the trace node
                 if (S.iR_tr >= 0 && S.iR_tr < n)  // (q - d_v) u at lo_{s+1}, flux on [c-h/2, c]
-                    S.sendR[P.par_out][go] = rob ? P.q_lo * xR - ((xR - xR1) * inv_h + half_h_dt * (xR - sm.rtr[1 * kColW + cc])) : xR;
+                    S.sendR[P.par_out][go] = rob ? S.tpR * xR - ((xR - xR1) * inv_h + half_h_dt * (xR - sm.rtr[1 * kColW + cc])) : xR;
                 else if (S.iR_tr == n)
                     S.sendR[P.par_out][go] = gh;
                 if (P.errIF) {

@@ -50,13 +50,14 @@ struct SubDev {
                        // -1 / n: the Dirichlet end node itself (no overlap)
     int ifL, ifR;      // U-line index of the lo / hi interface end node for err_if; -1 none
     int nblk;          // row blocks in use (<= C)
-    int pad_;
+    int grp;           // replica (batched parameter sweep): error slots errT/errIF + grp * err_stride
     double injL, injR;           // RHS weight of the incoming trace: a (Dirichlet) or 2 a h_v (Robin)
     double wt0, wt1, wb0, wb1;   // d_t (rows 0,1) and d_b (rows n-2, n-1)
     double Mi00, Mi01, Mi10, Mi11;  // (I_2 + D^T B^{-1} E)^{-1}
     double *slab[2];             // [(hi-lo+1)][nx], ping-pong by step parity
     const double *gL[2], *gR[2]; // incoming traces [nt][nx] by iteration parity
     double *sendL[2], *sendR[2]; // outgoing traces [nt][nx] by iteration parity
+    double tpL, tpR;             // Robin parameter of the trace sent left (p: it lands on a right end) and right (q)
 };
 
 struct StepParams {
@@ -64,6 +65,7 @@ struct StepParams {
     int nx, nv, nt;
     int n;                 // this launch computes level n+1
     int par_in, par_out;   // iteration parities of the traces read / written
+    int err_stride;        // error slots per replica (K_max)
     int par_in_lo;         // parity of the incoming LEFT trace: par_in (Jacobi) or par_out
                            // (Gauss-Seidel SWR1-SWR4: the left neighbour already ran this iteration)
     int from_u0;           // n == 0: u^0 from the u0 tables (no slab read)
@@ -74,8 +76,6 @@ struct StepParams {
     int qtab_len;
     int record;            // monodomain: record rows listed in line_of_node
     double q, a, qa, hv, dt, p;
-    double q_lo;           // Robin parameter of the left (lo) ends: q of OSWR(p, q) (= p for OSWR(p)); the
-                           // trace sent RIGHT lands on a left end and uses q_lo, the one sent left uses p
     double cf[kMaxRank];   // dt * ft[r][n+1]
     const double2 *rowc;   // per node: (1-|nu_j|, |nu_j|)
     const double *fv;      // [f_rank][nv+1]
@@ -506,7 +506,7 @@ __device__ __forceinline__ void write_traces(const StepParams &P, const Tile &t,
         double g = uc;
         if (P.send_robin) {  // (p + d_v) u with the half-cell flux on [c, c+h/2]
             const double up = xtr[kWarp + t.lane];
-            g = P.p * uc - ((uc - up) * inv_h + half_h_dt * (uc - rtr[t.lane]));
+            g = t.sd->tpL * uc - ((uc - up) * inv_h + half_h_dt * (uc - rtr[t.lane]));
         }
         S.sendL[P.par_out][off] = g;
     }
@@ -515,7 +515,7 @@ __device__ __forceinline__ void write_traces(const StepParams &P, const Tile &t,
         double g = uc;
         if (P.send_robin) {  // (q - d_v) u with the half-cell flux on [c-h/2, c]
             const double um = xtr[3 * kWarp + t.lane];
-            g = P.q_lo * uc - ((uc - um) * inv_h + half_h_dt * (uc - rtr[kWarp + t.lane]));
+            g = t.sd->tpR * uc - ((uc - um) * inv_h + half_h_dt * (uc - rtr[kWarp + t.lane]));
         }
         S.sendR[P.par_out][off] = g;
     }
@@ -566,8 +566,9 @@ __device__ __forceinline__ void block_err_flush(const StepParams &P, const Tile 
             a = fmax(a, sm.red[w]);
             b = fmax(b, sm.red[kMaxWarps + w]);
         }
-        if (a > 0.0 && P.errIF) atomic_max_pos(P.errIF, a);
-        if (b > 0.0 && P.errT) atomic_max_pos(P.errT, b);
+        const size_t go = static_cast<size_t>(t.sd->grp) * P.err_stride;
+        if (a > 0.0 && P.errIF) atomic_max_pos(P.errIF + go, a);
+        if (b > 0.0 && P.errT) atomic_max_pos(P.errT + go, b);
     }
 }
 

@@ -585,14 +585,14 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 if (tr_L && inblk(S.iL_tr)) {  // (p + d_v) u at hi_{s-1}, half-cell flux on [c, c+h/2]
                     const double uc = sm.xsp[lane];
                     double g = uc;
-                    if (P.send_robin) g = P.p * uc - ((uc - sm.xsp[kWarp + lane]) * inv_h + half_h_dt * (uc - sm.rtr[par][lane]));
+                    if (P.send_robin) g = S.tpL * uc - ((uc - sm.xsp[kWarp + lane]) * inv_h + half_h_dt * (uc - sm.rtr[par][lane]));
                     S.sendL[P.par_out][goff] = g;
                 }
                 if (tr_R && inblk(S.iR_tr)) {  // (q - d_v) u at lo_{s+1}, flux on [c-h/2, c]
                     const double uc = sm.xsp[2 * kWarp + lane];
                     double g = uc;
                     if (P.send_robin)
-                        g = P.q_lo * uc - ((uc - sm.xsp[3 * kWarp + lane]) * inv_h + half_h_dt * (uc - sm.rtr[par][kWarp + lane]));
+                        g = S.tpR * uc - ((uc - sm.xsp[3 * kWarp + lane]) * inv_h + half_h_dt * (uc - sm.rtr[par][kWarp + lane]));
                     S.sendR[P.par_out][goff] = g;
                 }
                 if (inblk(sp_row[4]))
@@ -626,8 +626,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 a = fmax(a, sm.red[c]);
                 b = fmax(b, sm.red[NW + c]);
             }
-            if (a > 0.0) atomic_max_pos(P.errIF, a);
-            if (b > 0.0 && P.errT) atomic_max_pos(P.errT, b);
+            const size_t go = static_cast<size_t>(S.grp) * P.err_stride;  // replica of this CTA's subdomain
+            if (a > 0.0) atomic_max_pos(P.errIF + go, a);
+            if (b > 0.0 && P.errT) atomic_max_pos(P.errT + go, b);
         }
     }
     KFP_T(63)

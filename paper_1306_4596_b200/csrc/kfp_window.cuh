@@ -453,14 +453,14 @@ __global__ void __launch_bounds__(P_ * kWarp, 1) step_window(const WinParams W) 
             if (tr_L && inblk(S.iL_tr)) {  // (p + d_v) u at hi_{s-1}, half-cell flux on [c, c+h/2]
                 const double uc = sm.xsp[lane];
                 double g = uc;
-                if (P.send_robin) g = P.p * uc - ((uc - sm.xsp[kWarp + lane]) * inv_h + half_h_dt * (uc - rtr[lane]));
+                if (P.send_robin) g = S.tpL * uc - ((uc - sm.xsp[kWarp + lane]) * inv_h + half_h_dt * (uc - rtr[lane]));
                 S.sendL[P.par_out][goff] = g;
             }
             if (tr_R && inblk(S.iR_tr)) {  // (q - d_v) u at lo_{s+1}, flux on [c-h/2, c]
                 const double uc = sm.xsp[2 * kWarp + lane];
                 double g = uc;
                 if (P.send_robin)
-                    g = P.q_lo * uc - ((uc - sm.xsp[3 * kWarp + lane]) * inv_h + half_h_dt * (uc - rtr[kWarp + lane]));
+                    g = S.tpR * uc - ((uc - sm.xsp[3 * kWarp + lane]) * inv_h + half_h_dt * (uc - rtr[kWarp + lane]));
                 S.sendR[P.par_out][goff] = g;
             }
             if (inblk(sp_row[4]))

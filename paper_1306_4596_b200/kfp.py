@@ -20,7 +20,8 @@ KIND = {"dirichlet": 0, "robin": 1}
 
 # Every symbol include/kfp.h declares (checked by tests/test_abi.py).
 SYMBOLS = (
-    "kfp_problem_create", "kfp_problem_destroy", "kfp_set_stream", "kfp_monodomain_solve", "kfp_swr_setup", "kfp_swr_setup_pq", "kfp_swr_solve_pq", "kfp_swr_set_schedule",
+    "kfp_problem_create", "kfp_problem_destroy", "kfp_set_stream", "kfp_monodomain_solve", "kfp_swr_setup", "kfp_swr_setup_pq", "kfp_swr_solve_pq", "kfp_swr_set_schedule", "kfp_swr_setup_batch",
+    "kfp_swr_batch_history", "kfp_swr_batch_subdomain_uT",
     "kfp_swr_reset", "kfp_swr_iterate", "kfp_swr_edge_buffers", "kfp_swr_bind_edge_buffers", "kfp_swr_solve", "kfp_error_history",
     "kfp_swr_subdomain_uT", "kfp_swr_subdomain_range", "kfp_swr_trace", "kfp_monodomain_uT", "kfp_launch_count",
     "kfp_plan", "kfp_last_timing", "kfp_last_error",
@@ -68,6 +69,9 @@ def load(path: str = LIB_PATH):
         "kfp_swr_setup": (i32, [vp, i32, dbl, i32, i32, i32, i32, i32]),
         "kfp_swr_setup_pq": (i32, [vp, i32, dbl, dbl, i32, i32, i32, i32, i32]),
         "kfp_swr_set_schedule": (i32, [vp, i32]),
+        "kfp_swr_setup_batch": (i32, [vp, i32, vp, vp, i32, i32, i32, i32]),
+        "kfp_swr_batch_history": (i32, [vp, i32, i32, vp, vp, vp]),
+        "kfp_swr_batch_subdomain_uT": (i32, [vp, i32, i32, vp]),
         "kfp_swr_solve_pq": (i32, [vp, i32, dbl, dbl, i32, i32, i32, vp]),
         "kfp_swr_reset": (i32, [vp]),
         "kfp_swr_iterate": (i32, [vp, i32]),
@@ -165,6 +169,28 @@ class Problem:
             _check(load().kfp_swr_setup_pq(self._h, KIND[kind], float(p), float(q), int(overlap), int(n_sub),
                                            int(s_begin), int(s_end), int(K_max)))
         self.n_sub, self.s_begin, self.s_end = n_sub, s_begin, s_end
+
+    def setup_batch(self, kind: str, ps, overlap: int, n_sub: int, K_max: int, qs=None):
+        """Batched parameter sweep: replica r runs OSWR(ps[r], qs[r]) (qs None: one-sided)."""
+        ps = np.ascontiguousarray(ps, dtype=np.float64)
+        qs = None if qs is None else np.ascontiguousarray(qs, dtype=np.float64)
+        _check(load().kfp_swr_setup_batch(self._h, KIND[kind], _ptr(ps), _ptr(qs), int(len(ps)), int(overlap),
+                                          int(n_sub), int(K_max)))
+        self.n_sub, self.s_begin, self.s_end, self.n_rep = n_sub, 0, n_sub, len(ps)
+
+    def batch_history(self, rep: int):
+        cap = 1 << 16
+        kk = ctypes.c_int32()
+        eT = np.zeros(cap)
+        eI = np.zeros(cap)
+        _check(load().kfp_swr_batch_history(self._h, int(rep), cap, ctypes.byref(kk), _ptr(eT), _ptr(eI)))
+        return eT[: kk.value].copy(), eI[: kk.value].copy()
+
+    def batch_subdomain_uT(self, rep: int, s: int):
+        lo, hi = self.subdomain_range(s)
+        out = np.empty((hi - lo + 1, self.grid.nx))
+        _check(load().kfp_swr_batch_subdomain_uT(self._h, int(rep), int(s), _ptr(out)))
+        return out
 
     def set_schedule(self, schedule: str):
         """'jacobi' (default after setup) or 'gauss_seidel' (the paper's SWR1-SWR4, single process)."""

@@ -296,3 +296,55 @@ def test_gauss_seidel_rejected_by_window_plan(kfp, monkeypatch):
         pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
         with pytest.raises(kfp.KfpError):
             pb.set_schedule("gauss_seidel")
+
+
+@pytest.mark.parametrize("two_sided", [False, True])
+def test_batched_parameter_sweep(kfp, two_sided):
+    """Batched Robin-parameter sweep (Fig. 1's experiment): every replica of one batched solve is
+    bitwise the individual solve with its (p, q) (the same per-tile arithmetic), and sampled replicas match
+    the oracle."""
+    import oracle
+
+    run = ki.config("c0").with_(K=6)
+    prob = ki.make_problem(run)
+    ps = [0.5, 1.0, 2.0, 4.0, 8.0, 16.0]
+    qs = [4.0, 0.7, 3.0, 1.0, 2.5, 0.3] if two_sided else None
+    with kfp.Problem(prob) as pb:
+        pb.setup_batch("robin", ps, 0, run.n_sub, run.K, qs=qs)
+        pb.reset()
+        pb.iterate(run.K)
+        batch = [(pb.batch_history(r), [pb.batch_subdomain_uT(r, s) for s in range(run.n_sub)]) for r in range(len(ps))]
+    for r, p in enumerate(ps):
+        q = None if qs is None else qs[r]
+        with kfp.Problem(prob) as pb:
+            pb.solve("robin", p, 0, run.n_sub, run.K, copy=False, q=q)
+            hist = pb.history()
+            slabs = [pb.subdomain_uT(s) for s in range(run.n_sub)]
+        (eT, eI), bs = batch[r]
+        assert np.array_equal(eT, hist[0]) and np.array_equal(eI, hist[1]), r
+        for a, b in zip(bs, slabs):
+            assert np.array_equal(a, b), r
+        if r in (0, 3):
+            ref = oracle.swr(prob, "robin", p, 0, run.n_sub, run.K, q=q)
+            assert rel(eT, ref["err_T"]) <= TOL and rel(eI, ref["err_if"]) <= TOL
+            for a, b in zip(bs, ref["uT_sub"]):
+                assert rel(a, b) <= TOL
+
+
+def test_batched_sweep_gauss_seidel(kfp):
+    import oracle
+
+    run = ki.scaled(ki.config("c1"), nt=200, K=4).with_(kind="robin", p=2.0, overlap=0, n_sub=4)
+    prob = ki.make_problem(run)
+    ps = [1.0, 3.0, 9.0]
+    with kfp.Problem(prob) as pb:
+        pb.setup_batch("robin", ps, 0, run.n_sub, run.K)
+        pb.set_schedule("gauss_seidel")
+        pb.reset()
+        pb.iterate(run.K)
+        for r, p in enumerate(ps):
+            ref = oracle.swr(prob, "robin", p, 0, run.n_sub, run.K, schedule="gauss_seidel")
+            eT, eI = pb.batch_history(r)
+            assert rel(eT, ref["err_T"]) <= TOL and rel(eI, ref["err_if"]) <= TOL
+            for s in range(run.n_sub):
+                assert rel(pb.batch_subdomain_uT(r, s), ref["uT_sub"][s]) <= TOL
