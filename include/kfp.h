@@ -136,6 +136,12 @@ kfp_status kfp_swr_set_schedule(kfp_problem pb, kfp_schedule schedule);
  * clear the error history. */
 kfp_status kfp_swr_reset(kfp_problem pb);
 
+/* Initial trace lambda^0 (SWR1 at k = 1; Table 1 uses a random one) of local interface i
+ * (between subdomains i and i+1, both on this process) in direction dir: 0 = toward subdomain i's right end,
+ * 1 = toward subdomain i+1's left end.  host: [nt][nx] fp64 (row n-1 = t_n), copied.  Must follow
+ * kfp_swr_reset (which zeroes them) and precede the first iteration; applies to every replica of a batch. */
+kfp_status kfp_swr_set_initial_trace(kfp_problem pb, int32_t i, int32_t dir, const double *host);
+
 /* Run n_iter Jacobi iterations on the local block (each: every local
  * subdomain solves the whole window [0,T] from u0 with the previous
  * iteration's traces, writes its outgoing traces and accumulates its errors;

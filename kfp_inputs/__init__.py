@@ -160,11 +160,24 @@ def random_forcing_problem(grid: Grid, seed: int = 0) -> Problem:
     return Problem(grid, *(np.ascontiguousarray(a) for a in (ft, fv, fx, u0v, u0x)), data="random")
 
 
+def zero_problem(grid: Grid) -> Problem:
+    """The error equation of the paper's experiments: f = 0, u0 = 0 (exact solution 0); the iterates
+    are then the SWR errors themselves, driven by the initial traces (Table 1: random lambda^0)."""
+    ft = np.zeros((1, grid.nt + 1))
+    fv = np.zeros((1, grid.nv + 1))
+    fx = np.zeros((1, grid.nx))
+    u0v = np.zeros((0, grid.nv + 1))
+    u0x = np.zeros((0, grid.nx))
+    return Problem(grid, ft, fv, fx, u0v, u0x, data="zero")
+
+
 def make_problem(run: Run) -> Problem:
     if run.data == "mms":
         return mms_problem(run.grid)
     if run.data == "random":
         return random_forcing_problem(run.grid)
+    if run.data == "zero":
+        return zero_problem(run.grid)
     raise ValueError(f"unknown data kind {run.data!r}")
 
 

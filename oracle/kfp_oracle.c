@@ -310,6 +310,7 @@ int orc_window(const orc_problem *P, int lo, int hi, int ltype, int rtype, doubl
  *                then toRight[i] (sent by i, used at lo_{i+1}); may be NULL.
  */
 static int swr_impl(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K, int gauss_seidel,
+                    const double *init_toL, const double *init_toR,
                     double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
     const int nx = P->nx, nt = P->nt, nv = P->nv, S = n_sub;
     if (S < 1 || nv % S != 0 || K < 1) return -1;
@@ -333,6 +334,9 @@ static int swr_impl(const orc_problem *P, int kind, double p, double q, int over
     double *toL_in = (double *)calloc((ni > 0 ? ni : 1) * TR, sizeof(double));
     double *toR_in = (double *)calloc((ni > 0 ? ni : 1) * TR, sizeof(double));
     double *toL_out = (double *)calloc((ni > 0 ? ni : 1) * TR, sizeof(double));
+    /* initial traces lambda^0: zero unless given (Table 1 uses random ones) */
+    if (init_toL && ni > 0) memcpy(toL_in, init_toL, sizeof(double) * ni * TR);
+    if (init_toR && ni > 0) memcpy(toR_in, init_toR, sizeof(double) * ni * TR);
     double *toR_out = (double *)calloc((ni > 0 ? ni : 1) * TR, sizeof(double));
     size_t tot = 0;
     for (int s = 0; s < S; ++s) tot += (size_t)(hi[s] - lo[s] + 1) * nx;
@@ -402,12 +406,20 @@ static int swr_impl(const orc_problem *P, int kind, double p, double q, int over
 }
 int orc_swr_pq(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K,
                double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
-    return swr_impl(P, kind, p, q, overlap, n_sub, K, 0, uT_sub, uT, UT, err_T, err_if, traces);
+    return swr_impl(P, kind, p, q, overlap, n_sub, K, 0, NULL, NULL, uT_sub, uT, UT, err_T, err_if, traces);
 }
 /* Gauss-Seidel schedule (the paper's serial SWR1-SWR4, subdomains in increasing v). */
 int orc_swr_gs(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K,
                double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
-    return swr_impl(P, kind, p, q, overlap, n_sub, K, 1, uT_sub, uT, UT, err_T, err_if, traces);
+    return swr_impl(P, kind, p, q, overlap, n_sub, K, 1, NULL, NULL, uT_sub, uT, UT, err_T, err_if, traces);
+}
+/* General form: schedule (0 Jacobi, 1 Gauss-Seidel) and initial traces init_toL / init_toR
+ * ([n_sub-1][nt][nx]: toward the left subdomain's right end / the right subdomain's left end; NULL = 0). */
+int orc_swr_ex(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K, int gauss_seidel,
+               const double *init_toL, const double *init_toR,
+               double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
+    return swr_impl(P, kind, p, q, overlap, n_sub, K, gauss_seidel, init_toL, init_toR, uT_sub, uT, UT, err_T, err_if,
+                    traces);
 }
 int orc_swr(const orc_problem *P, int kind, double p, int overlap, int n_sub, int K,
             double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {

@@ -1472,6 +1472,23 @@ kfp_status kfp_swr_reset(kfp_problem pb) {
     return KFP_OK;
 }
 
+kfp_status kfp_swr_set_initial_trace(kfp_problem pb, int32_t i, int32_t dir, const double *host) {
+    if (!pb || !pb->setup || i < pb->s_begin || i + 1 >= pb->s_end || dir < 0 || dir > 1 || !host || pb->k_done != 0) {
+        set_err("kfp_swr_set_initial_trace: interface %d not local, bad dir, or not right after a reset", i);
+        return KFP_E_INVAL;
+    }
+    const int nloc = pb->s_end - pb->s_begin;
+    const size_t bytes = sizeof(double) * (size_t)pb->nt * pb->nx;
+    for (int r = 0; r < pb->n_rep; ++r) {  // every replica of a batch starts from the same lambda^0
+        const SubDev &left = pb->subs[(size_t)r * nloc + (i - pb->s_begin)];
+        const SubDev &right = pb->subs[(size_t)r * nloc + (i + 1 - pb->s_begin)];
+        double *dst = const_cast<double *>(dir == 0 ? left.gR[0] : right.gL[0]);
+        KFP_CUDA(cudaMemcpyAsync(dst, host, bytes, cudaMemcpyHostToDevice, pb->stream));
+    }
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    return KFP_OK;
+}
+
 kfp_status kfp_swr_set_schedule(kfp_problem pb, kfp_schedule schedule) {
     if (!pb || !pb->setup) {
         set_err("kfp_swr_set_schedule: no setup");

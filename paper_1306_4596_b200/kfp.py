@@ -21,7 +21,7 @@ KIND = {"dirichlet": 0, "robin": 1}
 # Every symbol include/kfp.h declares (checked by tests/test_abi.py).
 SYMBOLS = (
     "kfp_problem_create", "kfp_problem_destroy", "kfp_set_stream", "kfp_monodomain_solve", "kfp_swr_setup", "kfp_swr_setup_pq", "kfp_swr_solve_pq", "kfp_swr_set_schedule", "kfp_swr_setup_batch",
-    "kfp_swr_batch_history", "kfp_swr_batch_subdomain_uT",
+    "kfp_swr_batch_history", "kfp_swr_batch_subdomain_uT", "kfp_swr_set_initial_trace",
     "kfp_swr_reset", "kfp_swr_iterate", "kfp_swr_edge_buffers", "kfp_swr_bind_edge_buffers", "kfp_swr_solve", "kfp_error_history",
     "kfp_swr_subdomain_uT", "kfp_swr_subdomain_range", "kfp_swr_trace", "kfp_monodomain_uT", "kfp_launch_count",
     "kfp_plan", "kfp_last_timing", "kfp_last_error",
@@ -72,6 +72,7 @@ def load(path: str = LIB_PATH):
         "kfp_swr_setup_batch": (i32, [vp, i32, vp, vp, i32, i32, i32, i32]),
         "kfp_swr_batch_history": (i32, [vp, i32, i32, vp, vp, vp]),
         "kfp_swr_batch_subdomain_uT": (i32, [vp, i32, i32, vp]),
+        "kfp_swr_set_initial_trace": (i32, [vp, i32, i32, vp]),
         "kfp_swr_solve_pq": (i32, [vp, i32, dbl, dbl, i32, i32, i32, vp]),
         "kfp_swr_reset": (i32, [vp]),
         "kfp_swr_iterate": (i32, [vp, i32]),
@@ -191,6 +192,12 @@ class Problem:
         out = np.empty((hi - lo + 1, self.grid.nx))
         _check(load().kfp_swr_batch_subdomain_uT(self._h, int(rep), int(s), _ptr(out)))
         return out
+
+    def set_initial_trace(self, i: int, direction: int, values):
+        """lambda^0 of local interface i toward the left subdomain's right end (0) / right subdomain's left end (1)."""
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        assert v.shape == (self.grid.nt, self.grid.nx)
+        _check(load().kfp_swr_set_initial_trace(self._h, int(i), int(direction), _ptr(v)))
 
     def set_schedule(self, schedule: str):
         """'jacobi' (default after setup) or 'gauss_seidel' (the paper's SWR1-SWR4, single process)."""

@@ -348,3 +348,31 @@ def test_batched_sweep_gauss_seidel(kfp):
             assert rel(eT, ref["err_T"]) <= TOL and rel(eI, ref["err_if"]) <= TOL
             for s in range(run.n_sub):
                 assert rel(pb.batch_subdomain_uT(r, s), ref["uT_sub"][s]) <= TOL
+
+
+@pytest.mark.parametrize("schedule", ["jacobi", "gauss_seidel"])
+def test_random_initial_traces(kfp, schedule):
+    """Random initial traces lambda^0 ('all the frequencies represented in the initial error') on the
+    error equation f = u0 = 0, as in the paper's Table 1 experiment: GPU vs oracle, both schedules."""
+    import oracle
+
+    run = ki.scaled(ki.config("c0"), nv=60, nt=40, K=6, t_final=0.1).with_(kind="robin", p=4.23, overlap=3, n_sub=3)
+    g = run.grid
+    prob = ki.zero_problem(g)
+    rng = np.random.default_rng(5)
+    toL = rng.uniform(-1, 1, size=(run.n_sub - 1, g.nt, g.nx))
+    toR = rng.uniform(-1, 1, size=(run.n_sub - 1, g.nt, g.nx))
+    with kfp.Problem(prob) as pb:
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        pb.set_schedule(schedule)
+        pb.reset()
+        for i in range(run.n_sub - 1):
+            pb.set_initial_trace(i, 0, toL[i])
+            pb.set_initial_trace(i, 1, toR[i])
+        pb.iterate(run.K)
+        eT, eI = pb.history()
+        slabs = [pb.subdomain_uT(s) for s in range(run.n_sub)]
+    r = oracle.swr(prob, run.kind, run.p, run.overlap, run.n_sub, run.K, schedule=schedule, init_traces=(toL, toR))
+    assert rel(eT, r["err_T"]) <= TOL and rel(eI, r["err_if"]) <= TOL
+    for a, b in zip(slabs, r["uT_sub"]):
+        assert rel(a, b) <= TOL
