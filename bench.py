@@ -271,7 +271,7 @@ def main():
     if world > 1 or args.gpus > 1:
         from paper_1306_4596_b200 import dist
 
-        return dist.bench_main(args, default_workload)
+        return dist.bench_main(args, default_workload, ClockSampler, measured_peaks)
     return bench_single(args)
 
 

@@ -90,10 +90,13 @@ def exchange(block, rank: int, world: int, parity: int):
             req.wait()
 
 
-def run_swr(block, K: int, rank: int, world: int):
-    """K Jacobi iterations with the edge exchange after each; returns the global (err_T, err_if)."""
+def run_swr(block, K: int, rank: int, world: int, on_iterate=None):
+    """K Jacobi iterations with the edge exchange after each; returns the global (err_T, err_if).
+    on_iterate(block) runs after each iteration's launches (e.g. to read the library's window timing)."""
     for k in range(1, K + 1):
         block.iterate()  # reads recv_*[(k-1)&1], writes send_*[k&1]
+        if on_iterate:
+            on_iterate(block)
         exchange(block, rank, world, k & 1)
     eT, eI = block.history()
     hist = torch.stack([eT, eI])
@@ -105,8 +108,12 @@ def run_swr(block, K: int, rank: int, world: int):
     return hist[0].numpy(), hist[1].numpy()
 
 
-def bench_main(args, default_workload):
-    """bench.py --gpus N under torchrun: the weak-scaling c4 family, one block of S/N subdomains per rank."""
+def bench_main(args, default_workload, clock_sampler=None, peaks=None):
+    """bench.py --gpus N under torchrun: the weak-scaling c4 family, one block of S/N subdomains per rank.
+    Prints (rank 0) the bench JSON line: device-timed value (max over ranks), the roofline of the step kernel
+    (algorithmic bytes per launch / average launch time, max over ranks), clocks sampled during the timed
+    region, and the end-to-end number through the public API (create from host tables, setup incl. the
+    monodomain reference, K iterations with the NCCL exchange, u(T) of the local subdomains back to the host)."""
     import json
 
     import numpy as np
@@ -117,47 +124,92 @@ def bench_main(args, default_workload):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # rank 0's stdout carries exactly one JSON line
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
     run = ki.config(args.workload or default_workload(world))
     g = run.grid
     prob = ki.make_problem(run)
-    blk = CudaBlock(prob, run.kind, run.p, run.overlap, run.n_sub, run.K * (args.steps + args.warmup) + 1, rank,
-                    world, local)
+    blk = CudaBlock(prob, run.kind, run.p, run.overlap, run.n_sub, run.K, rank, world, local)
     stream = torch.cuda.current_stream()
 
-    def one():
-        blk.reset()
-        run_swr(blk, run.K, rank, world)
+    kernel_ms = [0.0]
+
+    def tally(b):  # the step launches of the iteration just run (library events on the same stream)
+        kernel_ms[0] += b.pb.last_timing()[1]
+
+    def one(b, timed=False):
+        b.reset()
+        return run_swr(b, run.K, rank, world, tally if timed else None)
 
     for _ in range(args.warmup):
-        one()
+        one(blk)
     dist.barrier()
     torch.cuda.synchronize()
+    clocks = clock_sampler(local) if clock_sampler else None
+    if clocks:
+        clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = blk.pb.launch_count()
     e0.record(stream)
     for _ in range(args.steps):
-        one()
+        one(blk, timed=True)
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
+    clk = clocks.stop() if clocks else None
+    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)  # slowest rank
-    launches = torch.tensor([blk.pb.launch_count() - l0], device=f"cuda:{local}", dtype=torch.float64)
+    n_launch = blk.pb.launch_count() - l0
+    launches = torch.tensor([n_launch], device=dev, dtype=torch.float64)
     dist.all_reduce(launches, op=dist.ReduceOp.SUM)
+    # roofline of the step kernel on this rank: algorithmic bytes (16 B per unknown-row update) per launch
+    rows = sum(blk.pb.subdomain_range(s)[1] - blk.pb.subdomain_range(s)[0] + 1 for s in range(blk.s_begin, blk.s_end))
+    ends = 2 * (blk.s_end - blk.s_begin)  # end nodes that are not unknowns (Dirichlet / physical); Robin: upper bound
+    bytes_per_launch = 16.0 * g.nx * (rows - ends)
+    step_launches = g.nt * run.K * args.steps
+    per_launch = torch.tensor([kernel_ms[0] / 1e3 / step_launches], device=dev)
+    dist.all_reduce(per_launch, op=dist.ReduceOp.MAX)
+    plan = blk.pb.plan()
+    blk.close()
+
+    # end to end through the public API (host tables in, u(T) out), max over ranks
+    dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    b2 = CudaBlock(prob, run.kind, run.p, run.overlap, run.n_sub, run.K, rank, world, local)
+    hist = one(b2)
+    uT = [b2.subdomain_uT(s) for s in range(b2.s_begin, b2.s_end)]
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([f0.elapsed_time(f1)], device=dev)
+    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    d2h = sum(a.nbytes for a in uT) + hist[0].nbytes + hist[1].nbytes
+    h2d = prob.table_bytes()
+    b2.close()
     ms = float(ms.item())
     if rank == 0:
         value = run.updates * args.steps / (ms / 1e3)
+        achieved = bytes_per_launch / float(per_launch.item()) / 1e9
+        peak, peak_kind = peaks() if peaks else (None, None)
         line = {
             "metric": "grid-point updates/s (N_x*N_v*N_t*K / wall)", "value": value, "unit": "updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": run.name, "nx": g.nx, "nv": g.nv, "nt": g.nt, "K": run.K, "n_sub": run.n_sub,
-                       "kind": run.kind, "overlap": run.overlap, "parallelism": f"v-subdomain blocks x{world}, NCCL P2P",
-                       "l2": "inputs larger than L2"},
+                       "kind": run.kind, "overlap": run.overlap, "plan": plan,
+                       "parallelism": f"v-subdomain blocks x{world}, NCCL P2P",
+                       "l2": "inputs larger than L2", "updates_per_step": run.updates},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "kfp::step_fused_tma (rank 0 geometry, slowest rank's launch time)",
+                         "bytes_per_launch": bytes_per_launch, "avg_launch_us": float(per_launch.item()) * 1e6},
+            "e2e": {"value": run.updates / (float(e2e_ms.item()) / 1e3), "unit": "updates/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches.item()),
+            "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    blk.close()
     dist.barrier()
     dist.destroy_process_group()
     return 0
