@@ -41,7 +41,13 @@ __all__ = [
     "random_forcing_problem",
     "make_problem",
     "weak_scaling_config",
+    "fem_problem",
+    "paper_grid",
+    "SCHEMES",
 ]
+
+# The two discretisations the library implements; a problem names its own.
+SCHEMES = ("imex_fd", "split_fem")
 
 
 @dataclasses.dataclass(frozen=True)
@@ -75,6 +81,7 @@ class Problem:
     u0v: np.ndarray  # [u0_rank, nv+1]  (u0_rank may be 0)
     u0x: np.ndarray  # [u0_rank, nx]
     data: str = "mms"
+    scheme: str = "imex_fd"  # "imex_fd" (BASELINE.json north_star) | "split_fem" (the paper's, §3b)
 
     @property
     def f_rank(self) -> int:
@@ -169,6 +176,30 @@ def zero_problem(grid: Grid) -> Problem:
     u0v = np.zeros((0, grid.nv + 1))
     u0x = np.zeros((0, grid.nx))
     return Problem(grid, ft, fv, fx, u0v, u0x, data="zero")
+
+
+def fem_problem(grid: Grid, u0_seed: Optional[int] = None) -> Problem:
+    """Data of the paper's own experiments for the split-FEM scheme: the error
+    equation f = 0 (rank-0 forcing tables) and u0 = 0 -- the iterates are then driven by the initial traces
+    (random lambda^0) -- or, for parity cases, a rank-2 random u0 drawn from default_rng(u0_seed)
+    (u0v ~ N(0, 1), u0x ~ N(0, 1), in that order)."""
+    ft = np.zeros((0, grid.nt + 1))
+    fv = np.zeros((0, grid.nv + 1))
+    fx = np.zeros((0, grid.nx))
+    if u0_seed is None:
+        u0v = np.zeros((0, grid.nv + 1))
+        u0x = np.zeros((0, grid.nx))
+    else:
+        rng = np.random.default_rng(u0_seed)
+        u0v = rng.normal(size=(2, grid.nv + 1))
+        u0x = rng.normal(size=(2, grid.nx))
+    return Problem(grid, ft, fv, fx, u0v, u0x, data="zero" if u0_seed is None else "random_u0", scheme="split_fem")
+
+
+def paper_grid(j: int) -> Grid:
+    """The paper's Table 1 mesh at refinement level j: Delta t = h_x = h_v = 0.01 / 2^j on
+    x in [0,1), v in [-1,1], T = 2 -- N_x = 100 2^j, N_v = 200 2^j cells, N_t = 200 2^j steps."""
+    return Grid(100 * 2 ** j, 200 * 2 ** j, 200 * 2 ** j, 1.0, 2.0)
 
 
 def make_problem(run: Run) -> Problem:

@@ -8,7 +8,10 @@ with it; it takes its inputs from ``kfp_inputs`` like the CUDA path does.
 Contents
 --------
 * ``kfp_oracle.c`` (built into ``liborc.so``): the plain fp64 step-by-step
-  monodomain + Jacobi SWR solver (see its header for the paper passages).
+  monodomain + Jacobi / Gauss-Seidel SWR solver (see its header for the paper
+  passages), for both discretisations: the IMEX finite-difference scheme of
+  BASELINE.json's north_star and the paper's own split finite-element scheme
+  (``prob.scheme == "split_fem"``, P:443-525).
 * ``modal.py``: the mode-reduced oracle for the manufactured-solution configs
   (a special case that reduces the 2-D scheme to one complex 1-D recurrence
   per step, solved with LAPACK's banded solver).
@@ -53,7 +56,11 @@ class _Problem(ctypes.Structure):
         ("ft", ctypes.c_void_p), ("fv", ctypes.c_void_p), ("fx", ctypes.c_void_p),
         ("u0_rank", ctypes.c_int32),
         ("u0v", ctypes.c_void_p), ("u0x", ctypes.c_void_p),
+        ("scheme", ctypes.c_int32),
     ]
+
+
+SCHEME = {"imex_fd": 0, "split_fem": 1}
 
 
 def _load():
@@ -96,7 +103,8 @@ class _Bound:
         self.arrays = [np.ascontiguousarray(x, dtype=np.float64) for x in (prob.ft, prob.fv, prob.fx, prob.u0v, prob.u0x)]
         ft, fv, fx, u0v, u0x = self.arrays
         self.s = _Problem(g.nx, g.nv, g.nt, g.vmax, g.t_final, prob.f_rank,
-                          _ptr(ft), _ptr(fv), _ptr(fx), prob.u0_rank, _ptr(u0v), _ptr(u0x))
+                          _ptr(ft), _ptr(fv), _ptr(fx), prob.u0_rank, _ptr(u0v), _ptr(u0x),
+                          SCHEME[getattr(prob, "scheme", "imex_fd")])
 
     def ref(self):
         return ctypes.byref(self.s)

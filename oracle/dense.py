@@ -15,7 +15,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["dense_window", "dense_monodomain"]
+__all__ = ["dense_window", "dense_monodomain", "fem_matrices", "dense_fem_window"]
 
 
 def dense_window(prob, lo, hi, lkind="phys", rkind="phys", p=0.0, gL=None, gR=None, q=None):
@@ -104,3 +104,92 @@ def dense_window(prob, lo, hi, lkind="phys", rkind="phys", p=0.0, gL=None, gR=No
 def dense_monodomain(prob):
     """All time levels of the monodomain solution, [(nt+1), (nv+1), nx]."""
     return dense_window(prob, 0, prob.grid.nv)
+
+
+# ---------------------------------------------------------------------------
+# The paper's split finite-element scheme (P:443-525), brute force.
+#
+# Independent of kfp_oracle.c's window_fem(): the mass and stiffness matrices are
+# assembled by evaluating the hat functions (and their derivatives) at the three
+# Cavalieri-Simpson points of every cell (P:519-521 literally), the columns are
+# solved together by a dense LAPACK solve, and Step 2 evaluates the periodic
+# piecewise-linear interpolant of w at the foot of the characteristic x_m - tau v_j
+# with numpy.interp (P:456) instead of using the upwind weights.
+
+
+def _hat(v_nodes, i, v):
+    """P1 nodal basis function phi_i of the node set v_nodes evaluated at v (scalar)."""
+    h = v_nodes[1] - v_nodes[0]
+    return max(0.0, 1.0 - abs(v - v_nodes[i]) / h)
+
+
+def _dhat(v_nodes, i, v_left, v_right):
+    """d phi_i / dv on the open cell (v_left, v_right)."""
+    h = v_right - v_left
+    if abs(v_nodes[i] - v_left) < 1e-12 * h:
+        return -1.0 / h
+    if abs(v_nodes[i] - v_right) < 1e-12 * h:
+        return 1.0 / h
+    return 0.0
+
+
+def fem_matrices(v_nodes):
+    """M_ij = int phi_j phi_i dv and S_ij = int phi_j' phi_i' dv (eq. MMvS) over the span of
+    v_nodes, every cell integrated with the Cavalieri-Simpson rule."""
+    n = len(v_nodes)
+    M = np.zeros((n, n))
+    S = np.zeros((n, n))
+    for e in range(n - 1):
+        a, b = v_nodes[e], v_nodes[e + 1]
+        pts, wts = (a, 0.5 * (a + b), b), ((b - a) / 6.0, 4.0 * (b - a) / 6.0, (b - a) / 6.0)
+        for i in (e, e + 1):
+            for j in (e, e + 1):
+                M[i, j] += sum(w * _hat(v_nodes, i, x) * _hat(v_nodes, j, x) for x, w in zip(pts, wts))
+                S[i, j] += sum(w * _dhat(v_nodes, i, a, b) * _dhat(v_nodes, j, a, b) for x, w in zip(pts, wts))
+    return M, S
+
+
+def dense_fem_window(prob, lo, hi, lkind="phys", rkind="phys", p=0.0, gL=None, gR=None, q=None):
+    """Split-FEM window of subdomain [lo, hi]; returns (u [(nt+1), nn, nx], w [nt, nn, nx]) -- u^n after
+    every full step and w^{n+1/2}, the Step-1 results.  lkind/rkind: 'phys' (homogeneous Neumann,
+    P:435-436), 'dirichlet' (w = trace at the node), 'robin' ((q - d_v) w = trace at the left end,
+    (p + d_v) w = trace at the right end, through the boundary term of the weak form)."""
+    pl = p if q is None else q
+    g = prob.grid
+    nx, nt = g.nx, g.nt
+    dt = g.t_final / nt
+    tau = 0.5 * dt
+    v = g.v_nodes()[lo:hi + 1]
+    x = g.x_nodes()
+    nn = hi - lo + 1
+    M, S = fem_matrices(v)
+    A = M / tau + S
+    if lkind == "robin":
+        A[0, 0] += pl
+    if rkind == "robin":
+        A[-1, -1] += p
+    unknown = np.ones(nn, bool)
+    if lkind == "dirichlet":
+        unknown[0] = False
+    if rkind == "dirichlet":
+        unknown[-1] = False
+    Au = A[np.ix_(unknown, unknown)]
+    u = prob.u0_dense()[lo:hi + 1].copy()
+    us, ws = [u.copy()], []
+    for n in range(nt):
+        rhs = (M / tau) @ u
+        wv = np.zeros((nn, nx))
+        if lkind == "robin":
+            rhs[0] += gL[n]
+        if rkind == "robin":
+            rhs[-1] += gR[n]
+        if lkind == "dirichlet":
+            wv[0] = gL[n]
+        if rkind == "dirichlet":
+            wv[-1] = gR[n]
+        rhs = rhs - A[:, ~unknown] @ wv[~unknown]
+        wv[unknown] = np.linalg.solve(Au, rhs[unknown])
+        ws.append(wv.copy())
+        u = np.stack([np.interp(x - tau * v[j], x, wv[j], period=1.0) for j in range(nn)])
+        us.append(u.copy())
+    return np.array(us), np.array(ws)

@@ -31,6 +31,10 @@
  *       every iterate against the monodomain discrete solution (BASELINE.json
  *       north_star (c); a stopping diagnostic in the spirit of eq. (error),
  *       P:588-592).
+ * A second discretisation, the paper's own (operator splitting with
+ * consistent-mass linear finite elements in v, tau = dt/2, semi-Lagrangian
+ * transport, Neumann physical ends), is selected by orc_problem.scheme and
+ * implemented by window_fem() below; the SWR driver is shared.
  *
  * Layout of every 2-D array: v-major, element (node j, x-node m) at [j*nx + m].
  * Trace arrays [nt][nx]: row n-1 holds the value at t_n (n = 1..nt); the value
@@ -51,10 +55,12 @@ typedef struct {
     const double *ft, *fv, *fx;   /* ft[r*(nt+1)+n], fv[r*(nv+1)+j], fx[r*nx+m] */
     int32_t u0_rank;
     const double *u0v, *u0x;      /* u0v[r*(nv+1)+j], u0x[r*nx+m] */
+    int32_t scheme;               /* SCHEME_IMEX_FD or SCHEME_SPLIT_FEM (§3b) */
 } orc_problem;
 
 enum { END_PHYS = 0, END_DIRICHLET = 1, END_ROBIN = 2 };
 enum { KIND_DIRICHLET = 0, KIND_ROBIN = 1 };
+enum { SCHEME_IMEX_FD = 0, SCHEME_SPLIT_FEM = 1 };
 
 /* Grid spacings (readings R5/R6). */
 static double hx_of(const orc_problem *P) { return 1.0 / P->nx; }
@@ -95,6 +101,136 @@ static void thomas(int n, const double *sub, const double *diag, const double *s
     for (int i = n - 2; i >= 0; --i) x[i] = dp[i] - cp[i] * x[i + 1];
 }
 
+/* Window solve of one subdomain with the paper's own discretisation (DESIGN.md §3b,
+ * readings F1-F6).  Operator splitting, per step n -> n+1:
+ *   Step 1 (eq. step1): for every x-column m solve
+ *              (1/tau) M w + S w = (1/tau) M u^n
+ *          with M, S the P1 finite-element mass and stiffness matrices of eq. MMvS
+ *          on the subdomain's nodes, assembled element by element; the P1 element integrals are
+ *          integrated exactly by the Cavalieri-Simpson rule:
+ *              Me = h/6 [2 1; 1 2],   Se = 1/h [1 -1; -1 1].
+ *   Step 2 (eqs. step2_a / step2_b): u^{n+1}(x_m, v_j) = w(x_m - tau v_j, v_j) by linear
+ *          interpolation between the two x-nodes around the foot of the characteristic:
+ *              (1 - |v_j| tau/h_x) w_m + (|v_j| tau/h_x) w_{m-1}  (v_j > 0; m+1 for v_j < 0),
+ *          the weight of P:501 with the /h_x the formula drops (reading F3 = R7).
+ *   tau = dt/2 in both steps, dt = T/nt, as printed (reading F2).
+ * End nodes: END_PHYS = homogeneous Neumann: natural, nothing added to the weak form;
+ * END_ROBIN = the Robin condition imposed weakly through the boundary term of the weak form:
+ * left end (pl - d_v) w = g adds pl to the lo row's diagonal and g to its right-hand side, right
+ * end (pr + d_v) w = g likewise at hi; END_DIRICHLET = w = g at the node (its
+ * equation dropped, the known value moved to the neighbour's right-hand side).
+ * Outgoing traces (reading F4): Dirichlet: w_c.  Robin: p w_c - (the residual of the sender's
+ * half-row at c on the element toward the receiver's exterior), i.e. the flux the receiver's
+ * weak form needs, so that the monodomain solution is the fixed point (pinned).
+ * rec: w (the Step-1 result, where the transmission conditions act) at rec_nodes for every step;
+ * uT: u^{nt}, after the last Step 2.  Arguments as in window(). */
+static void window_fem(const orc_problem *P, int lo, int hi, int ltype, int rtype, double pl, double pr,
+                       const double *gL, const double *gR, int send_kind,
+                       int sendL_node, double *sendL, int sendR_node, double *sendR,
+                       int nrec, const int *rec_nodes, double *rec, double *uT) {
+    const int nx = P->nx, nt = P->nt, nn = hi - lo + 1;
+    const double hx = hx_of(P), hv = hv_of(P), dt = dt_of(P), tau = 0.5 * dt;
+    /* P1 element matrices on a cell of length hv (exact integrals) */
+    const double Me_d = hv / 3.0, Me_o = hv / 6.0, Se_d = 1.0 / hv, Se_o = -1.0 / hv;
+    /* global tridiagonal M and S on nodes lo..hi: *_d[i] diagonal of node lo+i, *_o[i] coupling (i, i+1) */
+    double *Md = (double *)calloc(nn, sizeof(double)), *Sd = (double *)calloc(nn, sizeof(double));
+    double *Mo = (double *)calloc(nn, sizeof(double)), *So = (double *)calloc(nn, sizeof(double));
+    for (int e = 0; e + 1 < nn; ++e) { /* element [lo+e, lo+e+1] */
+        Md[e] += Me_d; Md[e + 1] += Me_d; Mo[e] += Me_o;
+        Sd[e] += Se_d; Sd[e + 1] += Se_d; So[e] += Se_o;
+    }
+    double *u = (double *)malloc(sizeof(double) * (size_t)nn * nx);   /* u^n on all nodes */
+    double *w = (double *)malloc(sizeof(double) * (size_t)nn * nx);   /* Step-1 result */
+    for (int j = lo; j <= hi; ++j)
+        for (int m = 0; m < nx; ++m) u[(size_t)(j - lo) * nx + m] = initial(P, j, m);
+    const int first = (ltype == END_DIRICHLET) ? lo + 1 : lo;
+    const int last = (rtype == END_DIRICHLET) ? hi - 1 : hi;
+    const int nu = last - first + 1;
+
+    for (int n = 0; n < nt; ++n) {
+#pragma omp parallel
+        {
+            double *sub = (double *)malloc(sizeof(double) * (nu > 0 ? nu : 1));
+            double *diag = (double *)malloc(sizeof(double) * (nu > 0 ? nu : 1));
+            double *sup = (double *)malloc(sizeof(double) * (nu > 0 ? nu : 1));
+            double *rhs = (double *)malloc(sizeof(double) * (nu > 0 ? nu : 1));
+            double *cp = (double *)malloc(sizeof(double) * (nu > 0 ? nu : 1));
+            double *dp = (double *)malloc(sizeof(double) * (nu > 0 ? nu : 1));
+            double *x = (double *)malloc(sizeof(double) * (nu > 0 ? nu : 1));
+#pragma omp for schedule(static)
+            for (int m = 0; m < nx; ++m) {
+#define U_(j) u[(size_t)((j) - lo) * nx + m]
+#define W_(j) w[(size_t)((j) - lo) * nx + m]
+                const double left_val = (ltype == END_DIRICHLET) ? gL[(size_t)n * nx + m] : 0.0;
+                const double right_val = (rtype == END_DIRICHLET) ? gR[(size_t)n * nx + m] : 0.0;
+                for (int j = first; j <= last; ++j) {
+                    const int i = j - lo, r = j - first;
+                    /* row i of (1/tau) M w + S w = (1/tau) M u^n */
+                    double b = Md[i] * U_(j);
+                    if (i > 0) b += Mo[i - 1] * U_(j - 1);
+                    if (i < nn - 1) b += Mo[i] * U_(j + 1);
+                    rhs[r] = b / tau;
+                    diag[r] = Md[i] / tau + Sd[i];
+                    sub[r] = (i > 0) ? Mo[i - 1] / tau + So[i - 1] : 0.0;
+                    sup[r] = (i < nn - 1) ? Mo[i] / tau + So[i] : 0.0;
+                    if (j == lo && ltype == END_ROBIN) { /* (pl - d_v) w = g: boundary term of the weak form */
+                        diag[r] += pl;
+                        rhs[r] += gL[(size_t)n * nx + m];
+                    }
+                    if (j == hi && rtype == END_ROBIN) { /* (pr + d_v) w = g */
+                        diag[r] += pr;
+                        rhs[r] += gR[(size_t)n * nx + m];
+                    }
+                    if (j == lo + 1 && ltype == END_DIRICHLET) { rhs[r] -= sub[r] * left_val; sub[r] = 0.0; }
+                    if (j == hi - 1 && rtype == END_DIRICHLET) { rhs[r] -= sup[r] * right_val; sup[r] = 0.0; }
+                }
+                if (nu > 0) thomas(nu, sub, diag, sup, rhs, cp, dp, x);
+                for (int j = lo; j <= hi; ++j)
+                    W_(j) = (j < first) ? left_val : (j > last) ? right_val : x[j - first];
+                /* outgoing traces at step n+1 (reading F4) */
+                if (sendL_node >= 0) { /* to the left neighbour's right end: (pr + d_v) w, half-row on [c, c+1] */
+                    const int c = sendL_node;
+                    double g = W_(c);
+                    if (send_kind == KIND_ROBIN) {
+                        const double half = (Me_d * (W_(c) - U_(c)) + Me_o * (W_(c + 1) - U_(c + 1))) / tau +
+                                            Se_d * W_(c) + Se_o * W_(c + 1);
+                        g = pr * W_(c) - half;
+                    }
+                    sendL[(size_t)n * nx + m] = g;
+                }
+                if (sendR_node >= 0) { /* to the right neighbour's left end: (pl - d_v) w, half-row on [c-1, c] */
+                    const int c = sendR_node;
+                    double g = W_(c);
+                    if (send_kind == KIND_ROBIN) {
+                        const double half = (Me_d * (W_(c) - U_(c)) + Me_o * (W_(c - 1) - U_(c - 1))) / tau +
+                                            Se_d * W_(c) + Se_o * W_(c - 1);
+                        g = pl * W_(c) - half;
+                    }
+                    sendR[(size_t)n * nx + m] = g;
+                }
+#undef U_
+#undef W_
+            }
+            free(sub); free(diag); free(sup); free(rhs); free(cp); free(dp); free(x);
+        }
+        for (int i = 0; i < nrec; ++i)
+            memcpy(rec + ((size_t)i * nt + n) * nx, w + (size_t)(rec_nodes[i] - lo) * nx, sizeof(double) * nx);
+        /* Step 2: u^{n+1}(x_m, v_j) = w(x_m - tau v_j, v_j), linear interpolation in x */
+#pragma omp parallel for schedule(static)
+        for (int j = lo; j <= hi; ++j) {
+            const double v = v_of(P, j), c = fabs(v) * tau / hx;
+            const double *wr = w + (size_t)(j - lo) * nx;
+            double *ur = u + (size_t)(j - lo) * nx;
+            for (int m = 0; m < nx; ++m) {
+                const int nb = (v > 0.0) ? (m + nx - 1) % nx : (m + 1) % nx;  /* node on the foot's side */
+                ur[m] = (v == 0.0) ? wr[m] : (1.0 - c) * wr[m] + c * wr[nb];
+            }
+        }
+    }
+    if (uT) memcpy(uT, u, sizeof(double) * (size_t)nn * nx);
+    free(Md); free(Sd); free(Mo); free(So); free(u); free(w);
+}
+
 /* Window solve of one subdomain, nodes [lo, hi], from u0 over all nt steps
  * (one solve of SWR1 / SWR3, with the Jacobi data of P:594-597).
  *
@@ -119,6 +255,11 @@ static void window(const orc_problem *P, int lo, int hi, int ltype, int rtype, d
                    const double *gL, const double *gR, int send_kind,
                    int sendL_node, double *sendL, int sendR_node, double *sendR,
                    int nrec, const int *rec_nodes, double *rec, double *uT) {
+    if (P->scheme == SCHEME_SPLIT_FEM) {
+        window_fem(P, lo, hi, ltype, rtype, pl, pr, gL, gR, send_kind, sendL_node, sendL, sendR_node, sendR,
+                   nrec, rec_nodes, rec, uT);
+        return;
+    }
     const int nx = P->nx, nt = P->nt, nn = hi - lo + 1;
     const double hx = hx_of(P), hv = hv_of(P), dt = dt_of(P);
     const double a = dt / (hv * hv);
@@ -259,7 +400,8 @@ int orc_subdomains(int nv, int n_sub, int overlap, int32_t *lo, int32_t *hi) {
     return 0;
 }
 
-/* Monodomain solve on nodes [0, nv] with physical Dirichlet ends (BJ north_star
+/* Monodomain solve on nodes [0, nv] with physical ends (Dirichlet 0 for the IMEX FD scheme, Neumann for
+ * the split FEM scheme) (BJ north_star
  * (c): the reference every SWR iterate is compared with).  Records U at
  * rec_nodes for n = 1..nt and returns U(T). */
 int orc_monodomain(const orc_problem *P, int nrec, const int32_t *rec_nodes, double *rec, double *UT) {
