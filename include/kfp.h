@@ -64,6 +64,22 @@ typedef enum {
     KFP_GAUSS_SEIDEL = 1 /* the paper's serial SWR1-SWR4 */
 } kfp_schedule;
 
+/* Discretisation of a problem (fixed at creation; every later call follows it).
+ * KFP_SCHEME_IMEX_FD: BASELINE.json north_star's scheme: per step dt = T/nt, upwind
+ *   x-transport then one backward-Euler centred-FD v-solve (lumped-mass P1), forcing at t_{n+1},
+ *   Dirichlet 0 physical ends.
+ * KFP_SCHEME_SPLIT_FEM: the paper's own scheme: per step, Step 1 solves
+ *   (1/tau) M w + S w = (1/tau) M u^n with the consistent P1 mass and stiffness matrices (eq. MMvS),
+ *   Step 2 sets u^{n+1}(x, v) = w(x - tau v, v) by linear interpolation, tau = (t_final/nt)/2 in both
+ *   (P:452); homogeneous Neumann physical ends; Robin transmission imposed weakly; no
+ *   forcing (f_rank must be 0: the paper's error equation); requires tau/h_v^2 > 1/6 and
+ *   vmax*tau/h_x <= 1.  Interface errors (err_if) compare the Step-1 results w at the interface nodes;
+ *   u(T) and err_T are after the last Step 2. */
+typedef enum {
+    KFP_SCHEME_IMEX_FD = 0,
+    KFP_SCHEME_SPLIT_FEM = 1
+} kfp_scheme;
+
 /* Problem description (PAPER.md:33-38 data f, u0, T; grid per DESIGN.md R5/R6).
  * f(t_n, x_m, v_j) = sum_{r<f_rank} ft[r*(nt+1)+n] * fv[r*(nv+1)+j] * fx[r*nx+m]
  * u0(x_m, v_j)     = sum_{r<u0_rank} u0v[r*(nv+1)+j] * u0x[r*nx+m]   (u0_rank = 0: u0 = 0)
@@ -86,6 +102,12 @@ typedef struct {
  * *out is set only on success. */
 kfp_status kfp_problem_create(const kfp_problem_desc *desc, kfp_problem *out);
 
+/* As kfp_problem_create with an explicit discretisation (kfp_problem_create = KFP_SCHEME_IMEX_FD).
+ * KFP_SCHEME_SPLIT_FEM additionally returns KFP_E_INVAL for f_rank != 0 or tau/h_v^2 <= 1/6, and
+ * KFP_E_CFL for vmax*tau*nx > 1.  Its columns must fit the cluster kernel (<= 4224 unknown rows per
+ * subdomain and in the monodomain), else the setup / monodomain call returns KFP_E_INVAL. */
+kfp_status kfp_problem_create_ex(const kfp_problem_desc *desc, kfp_scheme scheme, kfp_problem *out);
+
 /* Free every device buffer and the handle (NULL is a no-op). */
 void kfp_problem_destroy(kfp_problem pb);
 
@@ -95,8 +117,8 @@ void kfp_problem_destroy(kfp_problem pb);
 kfp_status kfp_set_stream(kfp_problem pb, void *stream);
 
 /* Monodomain solve (the SWR reference, BJ north_star (c)): the same scheme on
- * nodes [0, nv] with physical Dirichlet ends.  uT: host [(nv+1)*nx] receiving
- * U(T), or NULL to keep it on the device only. */
+ * nodes [0, nv] with the scheme's physical ends (Dirichlet 0; split FEM: Neumann).
+ * uT: host [(nv+1)*nx] receiving U(T), or NULL to keep it on the device only. */
 kfp_status kfp_monodomain_solve(kfp_problem pb, double *uT);
 
 /* Configure a Jacobi SWR solve and allocate its buffers.

@@ -54,6 +54,7 @@ struct Plan {
     bool col = false;    // cluster-free column-tile kernel (kfp_col.cuh): 8 columns x the whole column per CTA
     bool window = false; // persistent pipelined window kernel (one launch per SWR iteration); implies fused geometry
     bool fused = false;  // fused TMA/cluster kernel; else the three-phase path
+    bool fem = false;    // the split-FEM instantiation of the fused kernel
     int P = 8, b = 32, R = 256, C = 1;
     int L = 0, B = 0, NR = 2;  // fused: chunk rows, register-array size (template), forcing ranks (template)
     int Gc_total = 1;          // fused: co-resident clusters (persistent grid size over all subdomains)
@@ -76,22 +77,30 @@ struct FusedData {
 };
 
 using FusedKernel = void (*)(const kfp::FusedParams);
-template <int B, int NR, int P>
+template <int B, int NR, int P, bool FEM = false>
 void fused_entry(FusedKernel *k, size_t *smem) {
-    *k = kfp::step_fused_tma<B, NR, P>;
-    *smem = kfp::fused_smem_bytes<B, NR, P>();
+    *k = kfp::step_fused_tma<B, NR, P, FEM>;
+    *smem = kfp::fused_smem_bytes<B, NR, P, FEM>();
 }
-// instantiated (B, NR, P) combinations of the fused kernel
-bool fused_kernel(int B, int NR, int P, FusedKernel *k, size_t *smem) {
-#define KFP_ENTRY(BB, NN, PP)             \
-    if (B == BB && NR == NN && P == PP) { \
-        fused_entry<BB, NN, PP>(k, smem); \
-        return true;                      \
+// instantiated (B, NR, P) combinations of the fused kernel; the split-FEM scheme (no forcing) uses NR = 2
+bool fused_kernel(int B, int NR, int P, FusedKernel *k, size_t *smem, bool fem = false) {
+#define KFP_ENTRY(BB, NN, PP)                        \
+    if (!fem && B == BB && NR == NN && P == PP) {    \
+        fused_entry<BB, NN, PP>(k, smem);            \
+        return true;                                 \
+    }
+#define KFP_FENTRY(BB, PP)                           \
+    if (fem && B == BB && NR == 2 && P == PP) {      \
+        fused_entry<BB, 2, PP, true>(k, smem);       \
+        return true;                                 \
     }
     KFP_ENTRY(8, 2, 8) KFP_ENTRY(16, 2, 8) KFP_ENTRY(17, 2, 8) KFP_ENTRY(32, 2, 8) KFP_ENTRY(33, 2, 8)
     KFP_ENTRY(8, 4, 8) KFP_ENTRY(16, 4, 8) KFP_ENTRY(17, 4, 8) KFP_ENTRY(32, 4, 8) KFP_ENTRY(33, 4, 8)
     KFP_ENTRY(32, 2, 16) KFP_ENTRY(33, 2, 16)
+    KFP_FENTRY(8, 8) KFP_FENTRY(16, 8) KFP_FENTRY(17, 8) KFP_FENTRY(32, 8) KFP_FENTRY(33, 8)
+    KFP_FENTRY(32, 16) KFP_FENTRY(33, 16)
 #undef KFP_ENTRY
+#undef KFP_FENTRY
     return false;
 }
 constexpr int kBs[] = {8, 16, 17, 32, 33};
@@ -140,8 +149,9 @@ bool col_kernel(int B, int NR, int P, ColKernel *k, size_t *smem) {
 // R = 16 L rows, C = ceil(n_max / R) <= 8 CTAs per cluster.  Otherwise the
 // three-phase path (P = 8, b = 32, block aggregates through global memory).
 Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool allow_window = false, int nx = 0,
-               bool allow_col = true) {
+               bool allow_col = true, bool fem = false) {
     Plan pl;
+    if (fem) allow_window = allow_col = false;  // the split-FEM scheme exists only in the per-step cluster kernel
     const int n_max = *std::max_element(ns.begin(), ns.end());
     const int NR = (f_rank <= 2) ? 2 : 4;
     // Column-tile kernel (opt-in, KFP_COL=1; correct, but measured slower than the cluster kernel on c2
@@ -237,8 +247,9 @@ Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool al
             }
         FusedKernel k;
         size_t smem = 0;
-        if (allow_fused && B > 0 && L <= 33 && f_rank <= kfp::kNRmax && fused_kernel(B, NR, P, &k, &smem)) {
+        if (allow_fused && B > 0 && L <= 33 && f_rank <= kfp::kNRmax && fused_kernel(B, NR, P, &k, &smem, fem)) {
             pl.fused = true;
+            pl.fem = fem;
             pl.P = P;
             pl.C = C;
             pl.L = L;
@@ -259,8 +270,8 @@ Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool al
     }
     char buf[200];
     if (pl.fused)
-        snprintf(buf, sizeof buf, "fused-tma-cluster P=%d L=%d (B=%d) R=%d C=%d NR=%d smem=%zu", pl.P, pl.L, pl.B, pl.R,
-                 pl.C, pl.NR, pl.smem);
+        snprintf(buf, sizeof buf, "fused-tma-cluster%s P=%d L=%d (B=%d) R=%d C=%d NR=%d smem=%zu", pl.fem ? "-fem" : "",
+                 pl.P, pl.L, pl.B, pl.R, pl.C, pl.NR, pl.smem);
     else
         snprintf(buf, sizeof buf, "three-phase P=%d b=%d R=%d C=%d smem=%zu", pl.P, pl.b, pl.R, pl.C, pl.smem);
     pl.text = buf;
@@ -299,6 +310,10 @@ struct kfp_problem_s {
     cudaStream_t own_stream = nullptr, stream = nullptr;
     int nx = 0, nv = 0, nt = 0;
     double vmax = 0, T = 0, hx = 0, hv = 0, dt = 0, a = 0, q = 0;
+    // scheme: KFP_SCHEME_IMEX_FD, or KFP_SCHEME_SPLIT_FEM: then dt = tau = T/(2 nt),
+    // a = tau/h_v^2 - 1/6 (the scaled off-diagonal of M/tau + S), ar = tau/h_v^2 (Robin / trace weight)
+    int scheme = KFP_SCHEME_IMEX_FD;
+    double ar = 0, dnu = 0, nu0 = 0;  // FD: ar = a.  FEM transport weight |j dnu + nu0| = |v_j| tau / h_x
     int f_rank = 0, u0_rank = 0;
     std::vector<double> ft;  // host [f_rank][nt+1]
     std::vector<double> fv_host;  // host [f_rank][nv+1]
@@ -391,20 +406,25 @@ void decompose(int nv, int S, int ov, std::vector<int> &lo, std::vector<int> &hi
 // Woodbury constants of one column system.
 // pl, pr: Robin parameters of the lo (left) and hi (right) end rows (OSWR(p, q): pl = q, pr = p).
 void woodbury(const kfp_problem pb, SubDev &sd, double pl, double pr) {
-    const long double a = pb->a, q = pb->q, h = pb->hv;
+    const long double a = pb->a, q = pb->q, h = pb->hv, ar = pb->ar;
     const int n = sd.n;
-    // d_t on rows (0,1), d_b on rows (n-2, n-1)
+    // d_t on rows (0,1), d_b on rows (n-2, n-1).  Unknown end rows (Robin, or the split-FEM scheme's
+    // Neumann ends = Robin with p = 0) are the doubled rows (1 + 2a + 2 ar p h) u_c - 2a u_{c-+1}.
+    if (sd.ltype == kfp::END_NEU) pl = 0.0;
+    if (sd.rtype == kfp::END_NEU) pr = 0.0;
+    const bool lrow = sd.ltype == kfp::END_ROBIN || sd.ltype == kfp::END_NEU;
+    const bool rrow = sd.rtype == kfp::END_ROBIN || sd.rtype == kfp::END_NEU;
     long double wt0, wt1, wb0, wb1;
-    if (sd.ltype == kfp::END_ROBIN) {
-        wt0 = a * (2.0L * pl * h + q);
+    if (lrow) {
+        wt0 = a * q + 2.0L * ar * pl * h;
         wt1 = -a;
     } else {
         wt0 = a * q;
         wt1 = 0.0L;
     }
-    if (sd.rtype == kfp::END_ROBIN) {
+    if (rrow) {
         wb0 = -a;
-        wb1 = 2.0L * a * pr * h;
+        wb1 = 2.0L * ar * pr * h;
     } else {
         wb0 = 0.0L;
         wb1 = 0.0L;
@@ -474,6 +494,8 @@ StepParams base_params(kfp_problem pb) {
     P.qa = pb->q / pb->a;
     P.hv = pb->hv;
     P.dt = pb->dt;
+    P.dnu = pb->dnu;
+    P.nu0 = pb->nu0;
     P.rowc = pb->d_rowc;
     P.fv = pb->d_fv;
     P.fx = pb->d_fx;
@@ -490,6 +512,9 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
                        int nrec = 0, const int *rec_rows = nullptr) {
     P.n = n;
     P.from_u0 = (n == 0);
+    // split FEM: step n transports w^{n-1/2} (the previous step's Step 2) before its Step 1; step 0 starts from u0
+    P.dnu = (n == 0) ? 0.0 : pb->dnu;
+    P.nu0 = (n == 0) ? 0.0 : pb->nu0;
     for (int r = 0; r < kfp::kMaxRank; ++r) P.cf[r] = (r < pb->f_rank) ? pb->dt * pb->ft[(size_t)r * (pb->nt + 1) + n + 1] : 0.0;
     P.P = pl.P;
     P.b = pl.b;
@@ -546,7 +571,7 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
         FP.tabs = fd.tabs;
         FusedKernel k;
         size_t smem;
-        fused_kernel(pl.B, pl.NR, pl.P, &k, &smem);
+        fused_kernel(pl.B, pl.NR, pl.P, &k, &smem, pl.fem);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(pl.C, FP.Gc, nsub);
         cfg.blockDim = block;
@@ -860,9 +885,13 @@ kfp_status build_tmaps(kfp_problem pb, const Plan &pl, const std::vector<SubDev>
     std::vector<CUtensorMap> maps(4 * ns);
     for (size_t i = 0; i < ns; ++i)
         for (int q = 0; q < 2; ++q) {
-            double *base = subs[i].slab[q] + (size_t)(subs[i].first - subs[i].lo) * pb->nx;
-            if (!make_tmap(&maps[2 * i + q], base, pb->nx, subs[i].n, pl.L) ||
-                !make_tmap(&maps[2 * ns + 2 * i + q], base, pb->nx, subs[i].n, pl.L, kfp::kWarp)) {
+            // FD: rows = the unknown rows, box L rows.  FEM: rows = every node of the slab, box L + 2 rows
+            // (the chunk and the rows above and below it; the kernel starts the box one row above)
+            const int off = pl.fem ? 0 : subs[i].first - subs[i].lo;
+            const int nrows = pl.fem ? subs[i].hi - subs[i].lo + 1 : subs[i].n, box = pl.fem ? pl.L + 2 : pl.L;
+            double *base = subs[i].slab[q] + (size_t)off * pb->nx;
+            if (!make_tmap(&maps[2 * i + q], base, pb->nx, nrows, box) ||
+                !make_tmap(&maps[2 * ns + 2 * i + q], base, pb->nx, nrows, box, kfp::kWarp)) {
                 set_err("cuTensorMapEncodeTiled failed (nx=%d rows=%d L=%d)", pb->nx, subs[i].n, pl.L);
                 return KFP_E_CUDA;
             }
@@ -918,7 +947,7 @@ kfp_status configure_kernels(Plan &pl) {
     } else if (pl.fused) {
         FusedKernel k;
         size_t smem;
-        fused_kernel(pl.B, pl.NR, pl.P, &k, &smem);
+        fused_kernel(pl.B, pl.NR, pl.P, &k, &smem, pl.fem);
         KFP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(pl.C, 1024, 1);
@@ -962,6 +991,21 @@ kfp_status alloc_general_scratch(kfp_problem pb, const Plan &pl, int nsub, doubl
     return KFP_OK;
 }
 
+// Split FEM: the window's last Step 2 for every subdomain in P.subs (nsub entries) -> the other slab
+// buffer, plus err_T against P.UT when set (kfp_fused.cuh fem_finish).
+kfp_status launch_fem_finish(kfp_problem pb, StepParams P, int nsub, int max_rows) {
+    P.dnu = pb->dnu;
+    P.nu0 = pb->nu0;
+    const int gy = std::max(1, std::min(max_rows, std::max(1, 4096 / std::max(1, nsub))));
+    kfp::fem_finish<<<dim3((pb->nx + 127) / 128, gy, nsub), 128, 0, pb->stream>>>(P);
+    pb->launches += 1;
+    KFP_CUDA(cudaGetLastError());
+    return KFP_OK;
+}
+
+// slab buffer that holds u(T) after a window: the last step's output (FD), or the fem_finish output
+int final_parity(const kfp_problem pb) { return (pb->nt + (pb->scheme == KFP_SCHEME_SPLIT_FEM ? 1 : 0)) & 1; }
+
 // Monodomain solve recording U at `lines` (BJ north_star (c)).
 kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     const size_t nx = pb->nx, nn = (size_t)pb->nv + 1;
@@ -984,17 +1028,22 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
 
     SubDev sd;
     std::memset(&sd, 0, sizeof sd);
+    const bool fem = pb->scheme == KFP_SCHEME_SPLIT_FEM;
     sd.lo = 0;
     sd.hi = pb->nv;
-    sd.first = 1;
-    sd.n = pb->nv - 1;
-    sd.ltype = sd.rtype = kfp::END_PHYS;
+    sd.first = fem ? 0 : 1;                 // FEM: Neumann ends, every node unknown
+    sd.n = fem ? pb->nv + 1 : pb->nv - 1;
+    sd.ltype = sd.rtype = fem ? kfp::END_NEU : kfp::END_PHYS;
     sd.iL_tr = sd.iR_tr = -2;
     sd.ifL = sd.ifR = -1;
     sd.slab[0] = pb->d_mono[0];
     sd.slab[1] = pb->d_mono[1];
     woodbury(pb, sd, 0.0, 0.0);
-    Plan pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true, false, pb->nx);
+    Plan pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true, false, pb->nx, true, fem);
+    if (fem && !pl.fused) {
+        set_err("monodomain: the split-FEM scheme needs the cluster kernel (column of %d rows > %d)", sd.n, 8 * 16 * 33);
+        return KFP_E_INVAL;
+    }
     sd.nblk = (sd.n + pl.R - 1) / pl.R;
     if (kfp_status st = ensure_qtab(pb, std::max(pl.R, sd.n) + 2)) return st;
     if (kfp_status st = configure_kernels(pl)) return st;
@@ -1025,6 +1074,11 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     }
     for (int n = 0; st == KFP_OK && n < pb->nt; ++n)
         st = launch_step(pb, pl, P, 1, n, fd, (int)rec_rows.size(), d_rec);
+    if (st == KFP_OK && fem) {  // U(T): the last Step 2 (no error slot)
+        P.UT = nullptr;
+        P.errT = nullptr;
+        st = launch_fem_finish(pb, P, 1, pb->nv + 1);
+    }
     cudaError_t e = cudaStreamSynchronize(pb->stream);
     cudaFree(d_sd);
     if (d_rec) cudaFree(d_rec);
@@ -1032,7 +1086,7 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     for (void *q : tmp2) cudaFree(q);
     if (st != KFP_OK) return st;
     KFP_CUDA(e);
-    pb->d_UT = pb->d_mono[pb->nt & 1];
+    pb->d_UT = pb->d_mono[final_parity(pb)];
     pb->mono_lines = lines;
     pb->mono_done = true;
     return KFP_OK;
@@ -1047,10 +1101,19 @@ extern "C" {
 const char *kfp_last_error(void) { return g_err.c_str(); }
 
 kfp_status kfp_problem_create(const kfp_problem_desc *d, kfp_problem *out) {
+    return kfp_problem_create_ex(d, KFP_SCHEME_IMEX_FD, out);
+}
+
+kfp_status kfp_problem_create_ex(const kfp_problem_desc *d, kfp_scheme scheme, kfp_problem *out) {
     if (!d || !out) {
         set_err("kfp_problem_create: NULL argument");
         return KFP_E_INVAL;
     }
+    if (scheme != KFP_SCHEME_IMEX_FD && scheme != KFP_SCHEME_SPLIT_FEM) {
+        set_err("kfp_problem_create: unknown scheme %d", (int)scheme);
+        return KFP_E_INVAL;
+    }
+    const bool fem = scheme == KFP_SCHEME_SPLIT_FEM;
     if (d->nx < 2 || d->nx % 2 || d->nv < 2 || d->nv % 2 || d->nt < 1 || !(d->vmax > 0) || !(d->t_final > 0) ||
         d->f_rank < 0 || d->f_rank > kfp::kMaxRank || d->u0_rank < 0 || d->u0_rank > kfp::kMaxRank) {
         set_err("kfp_problem_create: invalid sizes (nx=%d nv=%d nt=%d vmax=%g T=%g f_rank=%d u0_rank=%d); "
@@ -1062,11 +1125,26 @@ kfp_status kfp_problem_create(const kfp_problem_desc *d, kfp_problem *out) {
         set_err("kfp_problem_create: missing table pointer");
         return KFP_E_INVAL;
     }
-    const double hx = 1.0 / d->nx, dt = d->t_final / d->nt;
+    // split FEM: both sub-steps over tau = dt/2, no forcing (the paper's error
+    // equation), and tau/h_v^2 > 1/6 so that M/tau + S has negative off-diagonals (the
+    // kernel's constant-coefficient recurrence needs a = tau/h_v^2 - 1/6 > 0)
+    const double hx = 1.0 / d->nx, dt = d->t_final / d->nt * (fem ? 0.5 : 1.0);
     const double cfl = d->vmax * dt / hx;
     if (cfl > 1.0) {
-        set_err("kfp_problem_create: CFL Vmax*dt/h_x = %.6g > 1 (upwind step not a convex combination)", cfl);
+        set_err("kfp_problem_create: CFL Vmax*%s/h_x = %.6g > 1 (upwind step not a convex combination)",
+                fem ? "tau" : "dt", cfl);
         return KFP_E_CFL;
+    }
+    if (fem) {
+        const double hv = 2.0 * d->vmax / d->nv, r = dt / (hv * hv);
+        if (d->f_rank != 0) {
+            set_err("kfp_problem_create: the split-FEM scheme has no forcing term (P:602-605); f_rank must be 0");
+            return KFP_E_INVAL;
+        }
+        if (!(r > 1.0 / 6.0 + 1e-12)) {
+            set_err("kfp_problem_create: split FEM needs tau/h_v^2 > 1/6 (got %.6g)", r);
+            return KFP_E_INVAL;
+        }
     }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -1099,8 +1177,12 @@ kfp_status kfp_problem_create(const kfp_problem_desc *d, kfp_problem *out) {
     pb->hx = hx;
     pb->hv = 2.0 * d->vmax / d->nv;
     pb->dt = dt;
-    pb->a = dt / (pb->hv * pb->hv);
+    pb->scheme = scheme;
+    pb->ar = dt / (pb->hv * pb->hv);
+    pb->a = fem ? pb->ar - 1.0 / 6.0 : pb->ar;  // FEM: (M/tau + S) tau/h = tridiag(-a, 1 + 2a, -a)
     pb->q = ((1.0 + 2.0 * pb->a) - std::sqrt(1.0 + 4.0 * pb->a)) / (2.0 * pb->a);
+    pb->dnu = pb->hv * dt / hx;
+    pb->nu0 = -d->vmax * dt / hx;
     pb->f_rank = d->f_rank;
     pb->u0_rank = d->u0_rank;
     pb->ft.assign(d->ft, d->ft + (size_t)d->f_rank * (d->nt + 1));
@@ -1283,10 +1365,11 @@ kfp_status swr_setup_impl(kfp_problem pb, kfp_kind kind, const double *ps, const
         std::memset(&sd, 0, sizeof sd);
         sd.lo = pb->lo[s];
         sd.hi = pb->hi[s];
-        sd.ltype = (s == 0) ? kfp::END_PHYS : et;
-        sd.rtype = (s == n_sub - 1) ? kfp::END_PHYS : et;
-        sd.first = (sd.ltype == kfp::END_ROBIN) ? sd.lo : sd.lo + 1;
-        const int last = (sd.rtype == kfp::END_ROBIN) ? sd.hi : sd.hi - 1;
+        const int phys = (pb->scheme == KFP_SCHEME_SPLIT_FEM) ? kfp::END_NEU : kfp::END_PHYS;
+        sd.ltype = (s == 0) ? phys : et;
+        sd.rtype = (s == n_sub - 1) ? phys : et;
+        sd.first = (sd.ltype == kfp::END_ROBIN || sd.ltype == kfp::END_NEU) ? sd.lo : sd.lo + 1;
+        const int last = (sd.rtype == kfp::END_ROBIN || sd.rtype == kfp::END_NEU) ? sd.hi : sd.hi - 1;
         sd.n = last - sd.first + 1;
         // unknown-row index of the node whose trace is sent left / right; -2 = none.
         // Dirichlet without overlap sends its own end node (index -1 / n): the received value.
@@ -1294,8 +1377,8 @@ kfp_status swr_setup_impl(kfp_problem pb, kfp_kind kind, const double *ps, const
         sd.iR_tr = (s < n_sub - 1) ? pb->lo[s + 1] - sd.first : -2;
         sd.ifL = (s > 0) ? line_index(sd.lo) : -1;
         sd.ifR = (s < n_sub - 1) ? line_index(sd.hi) : -1;
-        sd.injL = (sd.ltype == kfp::END_ROBIN) ? 2.0 * pb->a * pb->hv : pb->a;
-        sd.injR = (sd.rtype == kfp::END_ROBIN) ? 2.0 * pb->a * pb->hv : pb->a;
+        sd.injL = (sd.ltype == kfp::END_ROBIN) ? 2.0 * pb->ar * pb->hv : (sd.ltype == kfp::END_DIRI) ? pb->a : 0.0;
+        sd.injR = (sd.rtype == kfp::END_ROBIN) ? 2.0 * pb->ar * pb->hv : (sd.rtype == kfp::END_DIRI) ? pb->a : 0.0;
         if (sd.n < 2) {
             set_err("kfp_swr_setup: subdomain %d has %d unknown rows (need >= 2)", s, sd.n);
             return KFP_E_INVAL;
@@ -1308,8 +1391,14 @@ kfp_status swr_setup_impl(kfp_problem pb, kfp_kind kind, const double *ps, const
     }
     std::vector<int> ns;
     for (const SubDev &sd : pb->subs) ns.push_back(sd.n);
-    pb->plan = make_plan(ns, pb->f_rank, true, n_rep == 1, pb->nx, n_rep == 1);
+    const bool fem = pb->scheme == KFP_SCHEME_SPLIT_FEM;
+    pb->plan = make_plan(ns, pb->f_rank, true, n_rep == 1, pb->nx, n_rep == 1, fem);
     Plan &pl = pb->plan;
+    if (fem && !pl.fused) {
+        set_err("kfp_swr_setup: the split-FEM scheme needs the cluster kernel (column of %d rows > %d)", n_max,
+                8 * 16 * 33);
+        return KFP_E_INVAL;
+    }
     // the rows of each outgoing trace stencil must sit in one row block
     for (int ii = 0; ii < ntot; ++ii) {
         const int i = ii % nloc;
@@ -1450,7 +1539,7 @@ kfp_status kfp_swr_batch_subdomain_uT(kfp_problem pb, int32_t rep, int32_t s, do
         return KFP_E_INVAL;
     }
     const SubDev &sd = pb->subs[(size_t)rep * pb->S + s];
-    KFP_CUDA(cudaMemcpyAsync(out, sd.slab[pb->nt & 1], sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
+    KFP_CUDA(cudaMemcpyAsync(out, sd.slab[final_parity(pb)], sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
                              cudaMemcpyDeviceToHost, pb->stream));
     KFP_CUDA(cudaStreamSynchronize(pb->stream));
     return KFP_OK;
@@ -1567,6 +1656,11 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
                 if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n, pb->fd)) return st;
             }
         }
+        if (pb->scheme == KFP_SCHEME_SPLIT_FEM) {  // u(T) = the last Step 2, and err_T
+            int rows = 0;
+            for (const SubDev &sd : pb->subs) rows = std::max(rows, sd.hi - sd.lo + 1);
+            if (kfp_status st = launch_fem_finish(pb, P, nloc, rows)) return st;
+        }
         KFP_CUDA(cudaEventRecord(pb->ev[3 + 2 * it], pb->stream));
         pb->k_done = k;
     }
@@ -1641,7 +1735,7 @@ kfp_status kfp_swr_solve_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
     if (kfp_status st = kfp_swr_iterate(pb, K)) return st;
     if (uT) {
         const size_t nx = pb->nx;
-        const int par = pb->nt & 1;
+        const int par = final_parity(pb);
         for (int s = 0; s < n_sub; ++s) {
             const SubDev &sd = pb->subs[s];
             const int c0 = s * (pb->nv / n_sub);
@@ -1691,7 +1785,7 @@ kfp_status kfp_swr_subdomain_uT(kfp_problem pb, int32_t s, double *out) {
         return KFP_E_INVAL;
     }
     const SubDev &sd = pb->subs[s - pb->s_begin];
-    KFP_CUDA(cudaMemcpyAsync(out, sd.slab[pb->nt & 1], sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
+    KFP_CUDA(cudaMemcpyAsync(out, sd.slab[final_parity(pb)], sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
                              cudaMemcpyDeviceToHost, pb->stream));
     KFP_CUDA(cudaStreamSynchronize(pb->stream));
     return KFP_OK;

@@ -39,7 +39,9 @@ constexpr int kWarp = 32;
 constexpr int kMaxRank = 4;
 constexpr int kMaxWarps = 16;
 constexpr int kMaxCluster = 16;
-enum : int { END_PHYS = 0, END_DIRI = 1, END_ROBIN = 2 };
+// END_NEU: homogeneous Neumann physical end of the split-FEM scheme -- an unknown end row
+// like END_ROBIN with p = 0 and no incoming trace
+enum : int { END_PHYS = 0, END_DIRI = 1, END_ROBIN = 2, END_NEU = 3 };
 
 // One subdomain as the kernels see it (global index s, nodes [lo, hi]).
 struct SubDev {
@@ -75,7 +77,8 @@ struct StepParams {
     int P, b, R, C;        // warps per CTA, rows per chunk, rows per block, blocks per column
     int qtab_len;
     int record;            // monodomain: record rows listed in line_of_node
-    double q, a, qa, hv, dt, p;
+    double q, a, qa, hv, dt, p;   // split FEM: a = tau/h_v^2 - 1/6, dt = tau
+    double dnu, nu0;       // split FEM transport weight of node j: |j dnu + nu0| = |v_j| tau / h_x (0 at n = 0)
     double cf[kMaxRank];   // dt * ft[r][n+1]
     const double2 *rowc;   // per node: (1-|nu_j|, |nu_j|)
     const double *fv;      // [f_rank][nv+1]

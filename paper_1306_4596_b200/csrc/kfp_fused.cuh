@@ -101,15 +101,18 @@ __host__ __device__ constexpr int fused_kq() {
     return ((P * B + 2) + 1) / 2 * 2;
 }
 
-template <int B, int NR, int P>
+// FEM (the paper's split scheme): the tile holds the chunk's rows plus the row above and
+// the row below (the 3-point mass average), and no per-row coefficient table (weights computed).
+template <int B, int NR, int P, bool FEM = false>
 struct FusedSmem {
-    static constexpr int kSlot = slot_doubles<B>();
+    static constexpr int kTileRows = B + (FEM ? 2 : 0);
+    static constexpr int kSlot = slot_doubles<kTileRows>();
     static constexpr int kRows = P * B;
     static constexpr int kCoef = 2 + NR;  // c0', c1', g_0' .. g_{NR-1}'
     static constexpr int kQ = fused_kq<B, P>();
     static constexpr int kTab = 2 * kQ + 2 * B;
-    alignas(128) double tile[P * kSlot];  // per warp: u^n rows [L][36]
-    alignas(16) double coef[kRows * kCoef];         // per warp: its chunk's rows of coefT
+    alignas(128) double tile[P * kSlot];  // per warp: u^n rows [L][36] (FEM: [L+2][36], rows cr0-1 .. cr0+L)
+    alignas(16) double coef[FEM ? 2 : kRows * kCoef];  // per warp: its chunk's rows of coefT
     alignas(16) double tab[kTab];                   // qp[kQ] | s2[kQ] | kr[2B]  (copy of FusedParams::tabs)
     alignas(16) double l2m[kL2M];                   // level-2 map of this (subdomain, block)
     double he[P * kCS];          // y at the chunk's last row (zero carry); then final Y carries
@@ -127,9 +130,9 @@ struct FusedSmem {
     uint64_t xbar[2];                      // cluster exchange, by tile parity
 };
 
-template <int B, int NR, int P>
+template <int B, int NR, int P, bool FEM = false>
 __host__ __device__ constexpr size_t fused_smem_bytes() {
-    return sizeof(FusedSmem<B, NR, P>);
+    return sizeof(FusedSmem<B, NR, P, FEM>);
 }
 
 // --------------------------------------------------------------------------- passes
@@ -163,6 +166,51 @@ __device__ __forceinline__ void pass_a_reg(const double *tile_w, const double *c
             h[l] = fma(q, hp, rp);
         }
         hp = h[l];
+    }
+    if (DIR != 0) hend = h[B - 1];
+}
+
+// Split-FEM pass A (P:480-516 reordered): the slab holds w^{n-1/2}; tile row i (node
+// jb + i, i = 0 .. B+1) is transported on the fly, u_i = w_i + nu_i (w_nb - w_i) with
+// nu_i = |vb + i dnu| = |v_j| tau / h_x (Step 2 of the previous step), and the right-hand side of
+// row l is the consistent-mass average (q/a)(u_{l-1} + 4 u_l + u_{l+1}) / 6 (Step 1, scaled by tau/h);
+// c1 = (q/a)/6, c4 = 4 c1.  Forward scan as in pass_a_reg.
+// Neumann / Robin end rows (unknown end node c): the doubled row's right-hand side (2 u_c + u_{c-+1}) / 3
+// is the interior average with the reflected ghost u_{c+-1} := u_{c-+1} -- the TRANSPORTED neighbour
+// (its own transport weight, not the ghost node's): gtop reflects at the chunk's first row, gl >= 0
+// at row gl (the column's last row; only ragged chunks, DIR = 0, hold it).
+template <int B, int DIR>
+__device__ __forceinline__ void pass_a_fem(const double *tile_w, int lane, double q, double c1, double c4, double vb,
+                                           double dnu, int jv2_0, double (&h)[B], int Lw, double &hend, bool gtop,
+                                           int gl) {
+    auto tr = [&](int i) -> double {
+        const double *row = tile_w + i * kTW + kHalo + lane;
+        const double w = row[0];
+        double nb;
+        if (DIR == 0) {
+            nb = row[(jv2_0 + 2 * i >= 0) ? -1 : 1];  // v_j >= 0: foot of the characteristic toward m-1
+        } else {
+            nb = row[DIR];
+        }
+        const double nu = fabs(fma(static_cast<double>(i), dnu, vb));
+        return fma(nu, nb - w, w);
+    };
+    double tm = tr(0), tc = tr(1), hp = 0.0;
+#pragma unroll
+    for (int l = 0; l < B; ++l) {
+        double tn = tr(l + 2);
+        if (DIR == 0 && l == gl) tn = tm;  // bottom ghost
+        if (l == 0 && gtop) tm = tn;       // top ghost
+        const double rp = fma(c4, tc, c1 * (tm + tn));
+        if (DIR == 0) {
+            h[l] = (l < Lw) ? fma(q, hp, rp) : 0.0;
+            hend = (l == Lw - 1) ? h[l] : hend;
+        } else {
+            h[l] = fma(q, hp, rp);
+        }
+        hp = h[l];
+        tm = tc;
+        tc = tn;
     }
     if (DIR != 0) hend = h[B - 1];
 }
@@ -242,11 +290,12 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 
 // --------------------------------------------------------------------------- the kernel
-template <int B, int NR, int P_>
+template <int B, int NR, int P_, bool FEM = false>
 __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const FusedParams FP) {
     constexpr int NW = P_;            // warps (= chunks) per CTA
     constexpr int kCPW = kWarp / NW;  // columns per warp in the transposed phase
-    using Sm = FusedSmem<B, NR, NW>;
+    constexpr int kX = FEM ? 1 : 0;   // FEM: extra tile rows above and below the chunk
+    using Sm = FusedSmem<B, NR, NW, FEM>;
     extern __shared__ __align__(128) char smraw[];
     Sm &sm = *reinterpret_cast<Sm *>(smraw);
     const StepParams &P = FP.S;
@@ -292,7 +341,12 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
 #pragma unroll
     for (int qq = 4; qq < 6; ++qq) cta_special |= inblk(sp_row[qq]);
     const int t_first = blockIdx.y;
-    const uint32_t tile_bytes = static_cast<uint32_t>(kTW * L * sizeof(double));
+    const uint32_t tile_bytes = static_cast<uint32_t>(kTW * (L + 2 * kX) * sizeof(double));
+    // tensor-map row of the tile's first row: FD maps start at the first unknown row, FEM maps at the
+    // slab's first node (the row above the chunk may be a Dirichlet end node)
+    const int ty0 = FEM ? cr0 + (S.first - S.lo) - 1 : cr0;
+    // node of tile row 0 (re-read from shared memory where used: not kept live across the tile loop)
+#define KFP_JB (S.first + cr0 - kX)
     KFP_T(0)
 
     // ---- prologue: barriers, constant tables (overlaps the previous step under PDL)
@@ -310,9 +364,13 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
         return;
     }
     if (lane == 0 && Lw > 0) { // this chunk's per-row coefficients (+ its first u^n tile below)
-        const uint32_t coef_bytes = static_cast<uint32_t>(Lw * Sm::kCoef * sizeof(double));
-        mbar_expect_tx(&sm.bar[warp], coef_bytes + (P.from_u0 ? 0u : tile_bytes));
-        bulk_g2s(coef_w, FP.coefT + static_cast<size_t>(S.first + cr0) * Sm::kCoef, coef_bytes, &sm.bar[warp]);
+        if (FEM) {
+            mbar_expect_tx(&sm.bar[warp], P.from_u0 ? 0u : tile_bytes);  // 0: completes phase 0 at once
+        } else {
+            const uint32_t coef_bytes = static_cast<uint32_t>(Lw * Sm::kCoef * sizeof(double));
+            mbar_expect_tx(&sm.bar[warp], coef_bytes + (P.from_u0 ? 0u : tile_bytes));
+            bulk_g2s(coef_w, FP.coefT + static_cast<size_t>(S.first + cr0) * Sm::kCoef, coef_bytes, &sm.bar[warp]);
+        }
     }
     if (threadIdx.x == 0) {    // q-power tables, pass-C coefficients, this block's level-2 map
         mbar_expect_tx(&sm.tbar, static_cast<uint32_t>((Sm::kTab + kL2M) * sizeof(double)));
@@ -321,7 +379,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
     }
     grid_dep_wait();  // the previous step's u^n is complete
     if (Lw > 0 && !P.from_u0 && lane == 0 && t_first < FP.ntiles)
-        tma_load_2d(tile_w, tmap, t_first * kWarp - kHalo, cr0, &sm.bar[warp]);
+        tma_load_2d(tile_w, tmap, t_first * kWarp - kHalo, ty0, &sm.bar[warp]);
     cluster_wait();  // matches the prologue arrive
     KFP_T(1)
 
@@ -337,8 +395,8 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
 #pragma unroll
         for (int r = 0; r < NR; ++r) fx[r] = (r < P.f_rank) ? P.cf[r] * __ldg(P.fx + r * P.nx + m) : 0.0;
         if (warp == 0) {  // incoming traces of this step (written by the previous iteration)
-            sm.gin[lane] = (S.ltype != END_PHYS) ? S.gL[P.par_in_lo][goff] : 0.0;
-            sm.gin[kWarp + lane] = (S.rtype != END_PHYS) ? S.gR[P.par_in][goff] : 0.0;
+            sm.gin[lane] = (S.ltype == END_DIRI || S.ltype == END_ROBIN) ? S.gL[P.par_in_lo][goff] : 0.0;
+            sm.gin[kWarp + lane] = (S.rtype == END_DIRI || S.rtype == END_ROBIN) ? S.gR[P.par_in][goff] : 0.0;
         }
 
         // ---- passes A and B (registers)
@@ -348,8 +406,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             if (!P.from_u0 || it == 0) mbar_wait(&sm.bar[warp], par);
             KFP_TT(0)
             if (P.from_u0) {  // u^0 from the separable u0 tables (0 B of HBM), incl. the halo columns
-                for (int l = 0; l < Lw; ++l) {
-                    const int j = S.first + cr0 + l;
+                for (int l = 0; l < Lw + 2 * kX; ++l) {
+                    const int j = KFP_JB + l;
+                    if (FEM && (j < S.lo || j > S.hi)) continue;  // ghost row outside the subdomain (set below)
                     for (int c = lane; c < kTW; c += kWarp) {
                         const int mm = ((m0 - kHalo + c) % P.nx + P.nx) % P.nx;
                         double s = 0.0;
@@ -361,27 +420,51 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 __syncwarp();
             } else if (m0 == 0 || m0 + w == P.nx) {
                 // periodic wrap of the halo at the ends of the x range (TMA zero-fills out-of-range columns)
-                const double *src = S.slab[P.n & 1] + static_cast<size_t>(S.first - S.lo + cr0) * P.nx;
+                const int jb = KFP_JB;
+                const double *src = S.slab[P.n & 1] + static_cast<ptrdiff_t>(jb - S.lo) * P.nx;
                 // one row per lane, strided: a chunk may hold more rows (L <= 33) than a warp has lanes
-                for (int l = lane; l < Lw; l += kWarp) {
-                    if (m0 == 0) tile_w[l * kTW + kHalo - 1] = src[static_cast<size_t>(l) * P.nx + P.nx - 1];
-                    if (m0 + w == P.nx) tile_w[l * kTW + kHalo + w] = src[static_cast<size_t>(l) * P.nx];
+                for (int l = lane; l < Lw + 2 * kX; l += kWarp) {
+                    if (FEM && (jb + l < S.lo || jb + l > S.hi)) continue;
+                    if (m0 == 0) tile_w[l * kTW + kHalo - 1] = src[static_cast<ptrdiff_t>(l) * P.nx + P.nx - 1];
+                    if (m0 + w == P.nx) tile_w[l * kTW + kHalo + w] = src[static_cast<ptrdiff_t>(l) * P.nx];
                 }
                 __syncwarp();
             }
-            const int jv2_0 = 2 * (S.first + cr0) - P.nv;      // 2 j - nv of the chunk's first row
-            const int jv2_1 = jv2_0 + 2 * (Lw - 1);
+            const int jb = KFP_JB;
+            const int jv2_0 = 2 * jb - P.nv;                   // 2 j - nv of the tile's first row
+            const int jv2_1 = jv2_0 + 2 * (Lw - 1 + 2 * kX);   // ... of its last row
             // full chunks take the unpredicated paths; the chunk holding the column's
             // last two rows takes the ragged one (it captures their k values)
             const bool full = (Lw == B) && (cr0 + Lw <= n - 2);
-            if (full && jv2_0 >= 0) pass_a_reg<B, NR, -1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
-            else if (full && jv2_1 < 0) pass_a_reg<B, NR, 1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
-            else pass_a_reg<B, NR, 0>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
+            if (FEM) {
+                const double c1 = P.qa * (1.0 / 6.0), c4 = 4.0 * c1, vb = fma(static_cast<double>(jb), P.dnu, P.nu0);
+                // unknown end nodes (Neumann / Robin ends) in this chunk: reflected ghosts
+                const bool gtop = cr0 == 0 && S.first == S.lo;
+                const int gl = (cr0 + Lw == n && S.first + n - 1 == S.hi) ? Lw - 1 : -1;
+                if (full && jv2_0 >= 0) pass_a_fem<B, -1>(tile_w, lane, q, c1, c4, vb, P.dnu, jv2_0, h, Lw, hend, gtop, gl);
+                else if (full && jv2_1 < 0) pass_a_fem<B, 1>(tile_w, lane, q, c1, c4, vb, P.dnu, jv2_0, h, Lw, hend, gtop, gl);
+                else pass_a_fem<B, 0>(tile_w, lane, q, c1, c4, vb, P.dnu, jv2_0, h, Lw, hend, gtop, gl);
+            } else {
+                if (full && jv2_0 >= 0) pass_a_reg<B, NR, -1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
+                else if (full && jv2_1 < 0) pass_a_reg<B, NR, 1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
+                else pass_a_reg<B, NR, 0>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
+            }
             if (trace_cta) {  // raw r (no incoming-trace term) at the outgoing-trace rows, for the Robin trace (R11)
 #pragma unroll
                 for (int side = 0; side < 2; ++side) {
                     const int itr = side ? S.iR_tr : S.iL_tr;
-                    if (itr >= 0 && inchunk(itr)) {
+                    if (FEM && itr >= 0 && inchunk(itr)) {
+                        // one-sided mass average (2 u_c + u_nb) / 3 of the transported rows at the trace node
+                        // c and its neighbour toward the sender's interior (reading F4)
+                        const int i = itr - cr0 + 1, inb = side ? i - 1 : i + 1, jb = KFP_JB;
+                        const double vb = fma(static_cast<double>(jb), P.dnu, P.nu0);
+                        auto trr = [&](int ii) {
+                            const double *row = tile_w + ii * kTW + kHalo + lane;
+                            const double nu = fabs(fma(static_cast<double>(ii), P.dnu, vb));
+                            return fma(nu, row[(2 * (jb + ii) - P.nv >= 0) ? -1 : 1] - row[0], row[0]);
+                        };
+                        sm.rtr[par][side * kWarp + lane] = (2.0 * trr(i) + trr(inb)) * (1.0 / 3.0);
+                    } else if (!FEM && itr >= 0 && inchunk(itr)) {
                         const int l = itr - cr0, j = S.first + itr;
                         const double2 rc = __ldg(P.rowc + j);
                         const double u = tile_w[l * kTW + kHalo + lane];
@@ -397,7 +480,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             if (lane == 0 && !P.from_u0 && t + FP.Gc < FP.ntiles) {
                 fence_proxy_async_smem();
                 mbar_expect_tx(&sm.bar[warp], tile_bytes);
-                tma_load_2d(tile_w, tmap, (t + FP.Gc) * kWarp - kHalo, cr0, &sm.bar[warp]);
+                tma_load_2d(tile_w, tmap, (t + FP.Gc) * kWarp - kHalo, ty0, &sm.bar[warp]);
             }
             if (full) {
                 kst = pass_b_full<B>(h, q);
@@ -536,7 +619,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                         if (l < Lw) dst[l * pitch] = h[l];
                 }
             }
-            if (P.last && active) {  // error at T on every unknown row (a 1/N_t fraction of the steps)
+            if (!FEM && P.last && active) {  // error at T on every unknown row (a 1/N_t fraction of the steps)
                 const double *ut = P.UT + static_cast<size_t>(S.first + cr0) * P.nx + m;
 #pragma unroll
                 for (int l = 0; l < B; ++l)
@@ -557,7 +640,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 const double g = sm.gin[lane];
                 if (S.iL_tr == -1) S.sendL[P.par_out][goff] = g;  // no overlap: the end node is the trace node
                 if (S.ifL >= 0) eif = fmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + m]));
-                if (P.last) {
+                if (FEM) {  // the node's value enters the next step's transport and mass average
+                    unew_slab[m] = g;
+                } else if (P.last) {
                     et = fmax(et, fabs(g - P.UT[static_cast<size_t>(S.lo) * P.nx + m]));
                     unew_slab[m] = g;
                 }
@@ -568,7 +653,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 const double g = sm.gin[kWarp + lane];
                 if (S.iR_tr == n) S.sendR[P.par_out][goff] = g;
                 if (S.ifR >= 0) eif = fmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + m]));
-                if (P.last) {
+                if (FEM) {
+                    unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + m] = g;
+                } else if (P.last) {
                     et = fmax(et, fabs(g - P.UT[static_cast<size_t>(S.hi) * P.nx + m]));
                     unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + m] = g;
                 }
@@ -585,14 +672,19 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 if (tr_L && inblk(S.iL_tr)) {  // (p + d_v) u at hi_{s-1}, half-cell flux on [c, c+h/2]
                     const double uc = sm.xsp[lane];
                     double g = uc;
-                    if (P.send_robin) g = S.tpL * uc - ((uc - sm.xsp[kWarp + lane]) * inv_h + half_h_dt * (uc - sm.rtr[par][lane]));
+                    if (P.send_robin) {
+                        const double xn = sm.xsp[kWarp + lane], xb = FEM ? (2.0 * uc + xn) * (1.0 / 3.0) : uc;
+                        g = S.tpL * uc - ((uc - xn) * inv_h + half_h_dt * (xb - sm.rtr[par][lane]));
+                    }
                     S.sendL[P.par_out][goff] = g;
                 }
                 if (tr_R && inblk(S.iR_tr)) {  // (q - d_v) u at lo_{s+1}, flux on [c-h/2, c]
                     const double uc = sm.xsp[2 * kWarp + lane];
                     double g = uc;
-                    if (P.send_robin)
-                        g = S.tpR * uc - ((uc - sm.xsp[3 * kWarp + lane]) * inv_h + half_h_dt * (uc - sm.rtr[par][kWarp + lane]));
+                    if (P.send_robin) {
+                        const double xn = sm.xsp[3 * kWarp + lane], xb = FEM ? (2.0 * uc + xn) * (1.0 / 3.0) : uc;
+                        g = S.tpR * uc - ((uc - xn) * inv_h + half_h_dt * (xb - sm.rtr[par][kWarp + lane]));
+                    }
                     S.sendR[P.par_out][goff] = g;
                 }
                 if (inblk(sp_row[4]))
@@ -632,6 +724,40 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
         }
     }
     KFP_T(63)
+}
+#undef KFP_JB
+
+// Split FEM: the slab after the window's last step holds w^{nt-1/2}; the scheme's
+// u(T) is its last Step 2, u_j(x_m) = w_j + nu_j (w_j(x_nb) - w_j(x_m)).  One pass over
+// every node of every listed subdomain: writes u(T) into the other slab buffer and, when UT is given,
+// max |u(T) - U(T)| into err_T (one atomic per CTA).  grid (ceil(nx / 128), row groups, nsub).
+__global__ void __launch_bounds__(128) fem_finish(const StepParams P) {
+    const SubDev &S = P.subs[blockIdx.z];
+    const int rows = S.hi - S.lo + 1, m = blockIdx.x * blockDim.x + threadIdx.x;
+    const double *src = S.slab[P.nt & 1];
+    double *dst = S.slab[(P.nt + 1) & 1];
+    double e = 0.0;
+    if (m < P.nx) {
+        const int ml = (m == 0) ? P.nx - 1 : m - 1, mr = (m == P.nx - 1) ? 0 : m + 1;
+        for (int r = blockIdx.y; r < rows; r += gridDim.y) {
+            const int j = S.lo + r;
+            const double *row = src + static_cast<size_t>(r) * P.nx;
+            const double w = row[m], wn = row[(2 * j - P.nv >= 0) ? ml : mr];
+            const double u = fma(fabs(fma(static_cast<double>(j), P.dnu, P.nu0)), wn - w, w);
+            dst[static_cast<size_t>(r) * P.nx + m] = u;
+            if (P.UT) e = fmax(e, fabs(u - P.UT[static_cast<size_t>(j) * P.nx + m]));
+        }
+    }
+    if (P.errT) {
+        __shared__ double red[4];
+        e = warp_max(e);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            e = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+            if (e > 0.0) atomic_max_pos(P.errT + static_cast<size_t>(S.grp) * P.err_stride, e);
+        }
+    }
 }
 
 }  // namespace kfp

@@ -17,10 +17,11 @@ LIB_PATH = os.environ.get("KFP_LIB_PATH") or os.path.join(_HERE, "libkfp.so")  #
 
 KFP_OK, KFP_E_INVAL, KFP_E_CFL, KFP_E_NOMEM, KFP_E_CUDA, KFP_E_STATE = 0, -1, -2, -3, -4, -6
 KIND = {"dirichlet": 0, "robin": 1}
+SCHEME = {"imex_fd": 0, "split_fem": 1}  # kfp_scheme (include/kfp.h)
 
 # Every symbol include/kfp.h declares (checked by tests/test_abi.py).
 SYMBOLS = (
-    "kfp_problem_create", "kfp_problem_destroy", "kfp_set_stream", "kfp_monodomain_solve", "kfp_swr_setup", "kfp_swr_setup_pq", "kfp_swr_solve_pq", "kfp_swr_set_schedule", "kfp_swr_setup_batch",
+    "kfp_problem_create", "kfp_problem_create_ex", "kfp_problem_destroy", "kfp_set_stream", "kfp_monodomain_solve", "kfp_swr_setup", "kfp_swr_setup_pq", "kfp_swr_solve_pq", "kfp_swr_set_schedule", "kfp_swr_setup_batch",
     "kfp_swr_batch_history", "kfp_swr_batch_subdomain_uT", "kfp_swr_set_initial_trace",
     "kfp_swr_reset", "kfp_swr_iterate", "kfp_swr_edge_buffers", "kfp_swr_bind_edge_buffers", "kfp_swr_solve", "kfp_error_history",
     "kfp_swr_subdomain_uT", "kfp_swr_subdomain_range", "kfp_swr_trace", "kfp_monodomain_uT", "kfp_launch_count",
@@ -63,6 +64,7 @@ def load(path: str = LIB_PATH):
     ppd = ctypes.POINTER(ctypes.c_void_p)
     sig = {
         "kfp_problem_create": (i32, [ctypes.POINTER(_Desc), ctypes.POINTER(vp)]),
+        "kfp_problem_create_ex": (i32, [ctypes.POINTER(_Desc), i32, ctypes.POINTER(vp)]),
         "kfp_problem_destroy": (None, [vp]),
         "kfp_set_stream": (i32, [vp, vp]),
         "kfp_monodomain_solve": (i32, [vp, vp]),
@@ -108,9 +110,10 @@ def _ptr(a: Optional[np.ndarray]):
 
 class Problem:
     """One problem on one device (``kfp_problem``).  ``prob`` is a ``kfp_inputs.Problem``-like object
-    (``grid`` with nx, nv, nt, vmax, t_final and tables ft, fv, fx, u0v, u0x)."""
+    (``grid`` with nx, nv, nt, vmax, t_final and tables ft, fv, fx, u0v, u0x).  The discretisation is
+    ``scheme`` if given, else ``prob.scheme`` (default "imex_fd"; "split_fem" is the paper's own)."""
 
-    def __init__(self, prob, device: int = 0):
+    def __init__(self, prob, device: int = 0, scheme: Optional[str] = None):
         lib = load()
         g = prob.grid
         self.grid = g
@@ -119,7 +122,8 @@ class Problem:
         d = _Desc(g.nx, g.nv, g.nt, g.vmax, g.t_final, ft.shape[0], _ptr(ft), _ptr(fv), _ptr(fx),
                   u0v.shape[0], _ptr(u0v), _ptr(u0x), device)
         h = ctypes.c_void_p()
-        _check(lib.kfp_problem_create(ctypes.byref(d), ctypes.byref(h)))
+        self.scheme = scheme or getattr(prob, "scheme", "imex_fd")
+        _check(lib.kfp_problem_create_ex(ctypes.byref(d), SCHEME[self.scheme], ctypes.byref(h)))
         self._h = h
         self.h2d_bytes = int(sum(t.nbytes for t in tabs))
         self.n_sub = None

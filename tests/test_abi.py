@@ -63,6 +63,26 @@ def test_create_validation_without_device(lib):
         assert e.value.status == kfp.KFP_E_CUDA
 
 
+def test_split_fem_validation_without_device(lib):
+    """The split-FEM scheme rejects forcing, tau/h_v^2 <= 1/6 and vmax tau/h_x > 1 before
+    any device work."""
+    import dataclasses
+
+    import kfp_inputs as ki
+    from paper_1306_4596_b200 import kfp
+
+    g = ki.paper_grid(0)
+    with pytest.raises(kfp.KfpError) as e:  # forcing given
+        kfp.Problem(ki.mms_problem(g), scheme="split_fem")
+    assert e.value.status == kfp.KFP_E_INVAL
+    with pytest.raises(kfp.KfpError) as e:  # tau / h_v^2 = 5e-6 / 0.1^2 = 5e-4 <= 1/6
+        kfp.Problem(ki.fem_problem(dataclasses.replace(g, nv=20, nt=200000)))
+    assert e.value.status == kfp.KFP_E_INVAL
+    with pytest.raises(kfp.KfpError) as e:  # vmax tau / h_x = 1 * 0.1 * 100 = 10 > 1
+        kfp.Problem(ki.fem_problem(dataclasses.replace(g, nt=10)))
+    assert e.value.status == kfp.KFP_E_CFL
+
+
 def test_product_path_does_not_import_oracle():
     """The product package never imports the oracle (and vice versa)."""
     pkg = os.path.join(ROOT, "paper_1306_4596_b200")
