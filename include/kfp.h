@@ -224,6 +224,32 @@ kfp_status kfp_swr_solve_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
  * iteration. */
 kfp_status kfp_error_history(kfp_problem pb, int32_t cap, int32_t *K_out, double *err_T, double *err_if);
 
+/* Error quantities an iteration records (per replica, per iteration k = 1..K):
+ *  KFP_ERR_T       err_T[k]  = max over every node of every subdomain of |u_s^k(T) - U(T)|;
+ *  KFP_ERR_IF      err_if[k] = max over each subdomain's interface end nodes and all steps of |u_s^k - U|;
+ *  KFP_ERR_OVERLAP err_ov[k] = max over every closed overlap [lo_{s+1}, hi_s], all steps and x-nodes of
+ *                  |u_s^k - u_{s+1}^k| -- the paper's convergence test (eq. 'error'); only with
+ *                  kfp_swr_set_overlap_error(pb, 1), only interfaces whose two subdomains are local.
+ * (Split FEM: err_if and err_ov use the Step-1 values w, where the transmission conditions act.) */
+typedef enum { KFP_ERR_T = 0, KFP_ERR_IF = 1, KFP_ERR_OVERLAP = 2 } kfp_metric;
+
+/* Turn the overlap recording of KFP_ERR_OVERLAP on (1) or off (0) for the current setup.  On first use it
+ * allocates, per local interface and side, (hi_s - lo_{s+1} + 1) * nt * nx doubles of device memory; every
+ * step then also stores the subdomains' overlap rows (Dirichlet end nodes from the incoming trace), and
+ * every iteration ends with one reduction launch.  KFP_E_STATE before a setup; KFP_E_INVAL unless the plan
+ * is the per-step cluster kernel (not KFP_WINDOW / KFP_COL / the three-phase path). */
+kfp_status kfp_swr_set_overlap_error(kfp_problem pb, int32_t on);
+
+/* err_ov history of replica `rep` (0 for an ordinary setup): as kfp_error_history.  KFP_E_STATE if the
+ * recording is off or no iteration ran. */
+kfp_status kfp_swr_overlap_history(kfp_problem pb, int32_t rep, int32_t cap, int32_t *K_out, double *err_ov);
+
+/* Tolerance stopping: run single iterations until `metric` of the last one (replica 0) is
+ * below eps (or not finite), or k_max more iterations have run; *k_out = iterations done since the last
+ * reset.  Each iteration synchronises the stream once to read its error (8 bytes).  KFP_E_STATE if
+ * k_done + k_max > K_max or KFP_ERR_OVERLAP without recording. */
+kfp_status kfp_swr_iterate_until(kfp_problem pb, kfp_metric metric, double eps, int32_t k_max, int32_t *k_out);
+
 /* Copy the local subdomain s's current u_s(T) slab [(hi_s-lo_s+1)*nx] to host
  * memory (s is the global subdomain index, s_begin <= s < s_end). */
 kfp_status kfp_swr_subdomain_uT(kfp_problem pb, int32_t s, double *out);

@@ -83,7 +83,7 @@ def _load():
                                        ctypes.c_int, dp, dp, dp, dp, dp, dp]
             lib.orc_swr_gs.argtypes = lib.orc_swr_pq.argtypes
             lib.orc_swr_ex.argtypes = [P, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int,
-                                       ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp, dp, dp]
+                                       ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp, dp, dp, dp]
             lib.orc_window_pq.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                           ctypes.c_double, dp, dp, ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, dp,
                                           ctypes.c_int, dp, dp, dp]
@@ -153,7 +153,8 @@ def window(prob, lo, hi, ltype, rtype, p, gL, gR, send_kind, sendL_node=-1, send
 
 def swr(prob, kind: str, p: float, overlap: int, n_sub: int, K: int, want_traces: bool = False, q=None,
         schedule: str = "jacobi", init_traces=None):
-    """Jacobi SWR; returns dict(uT, uT_sub (list of slabs), UT, err_T, err_if, traces, lo, hi).
+    """Jacobi SWR; returns dict(uT, uT_sub (list of slabs), UT, err_T, err_if, err_ov, traces, lo, hi); err_ov is
+    the paper's convergence quantity (eq. 'error'): max over the closed overlaps of |u_s - u_{s+1}|.
     Robin: OSWR(p, q) with p on every right end and q (default p: one-sided OSWR(p)) on every left end.
     schedule: "jacobi" (parallel) or "gauss_seidel" (the paper's SWR1-SWR4).
     init_traces: None (zero lambda^0) or (toL, toR), each [n_sub-1, nt, nx]: the initial traces toward the left
@@ -167,13 +168,14 @@ def swr(prob, kind: str, p: float, overlap: int, n_sub: int, K: int, want_traces
     UT = np.zeros((g.nv + 1, g.nx))
     err_T = np.zeros(K)
     err_if = np.zeros(K)
+    err_ov = np.zeros(K)
     traces = np.zeros((max(2 * (n_sub - 1), 1), g.nt, g.nx)) if want_traces else None
     gs = {"jacobi": 0, "gauss_seidel": 1}[schedule]
     iL = iR = None
     if init_traces is not None:
         iL, iR = (np.ascontiguousarray(a, dtype=np.float64).reshape(n_sub - 1, g.nt, g.nx) for a in init_traces)
     rc = _load().orc_swr_ex(b.ref(), KIND[kind], p, p if q is None else q, overlap, n_sub, K, gs, _ptr(iL), _ptr(iR),
-                            _ptr(uT_sub), _ptr(uT), _ptr(UT), _ptr(err_T), _ptr(err_if), _ptr(traces))
+                            _ptr(uT_sub), _ptr(uT), _ptr(UT), _ptr(err_T), _ptr(err_if), _ptr(traces), _ptr(err_ov))
     if rc != 0:
         raise ValueError("orc_swr rejected the arguments")
     slabs, off = [], 0
@@ -181,5 +183,5 @@ def swr(prob, kind: str, p: float, overlap: int, n_sub: int, K: int, want_traces
         n = (h - l + 1) * g.nx
         slabs.append(uT_sub[off:off + n].reshape(h - l + 1, g.nx))
         off += n
-    return dict(uT=uT, uT_sub=slabs, UT=UT, err_T=err_T, err_if=err_if,
+    return dict(uT=uT, uT_sub=slabs, UT=UT, err_T=err_T, err_if=err_if, err_ov=err_ov,
                 traces=None if traces is None else traces[: 2 * (n_sub - 1)], lo=lo, hi=hi)

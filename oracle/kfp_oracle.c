@@ -453,7 +453,8 @@ int orc_window(const orc_problem *P, int lo, int hi, int ltype, int rtype, doubl
  */
 static int swr_impl(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K, int gauss_seidel,
                     const double *init_toL, const double *init_toR,
-                    double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
+                    double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces,
+                    double *err_ov) {
     const int nx = P->nx, nt = P->nt, nv = P->nv, S = n_sub;
     if (S < 1 || nv % S != 0 || K < 1) return -1;
     int32_t *lo = (int32_t *)malloc(sizeof(int32_t) * S), *hi = (int32_t *)malloc(sizeof(int32_t) * S);
@@ -483,7 +484,13 @@ static int swr_impl(const orc_problem *P, int kind, double p, double q, int over
     size_t tot = 0;
     for (int s = 0; s < S; ++s) tot += (size_t)(hi[s] - lo[s] + 1) * nx;
     double *slabs = (double *)malloc(sizeof(double) * tot);
-    double *rec = (double *)malloc(sizeof(double) * 2 * TR);
+    /* overlap records for the paper's stopping quantity (eq. 'error'): interface i's closed
+     * overlap [lo_{i+1}, hi_i] as seen by subdomain i (ovA) and by i+1 (ovB) */
+    int ovmax = 1;
+    for (int i = 0; i + 1 < S; ++i) if (hi[i] - lo[i + 1] + 1 > ovmax) ovmax = hi[i] - lo[i + 1] + 1;
+    double *rec = (double *)malloc(sizeof(double) * (2 + 2 * (size_t)ovmax) * TR);
+    double *ovA = err_ov ? (double *)malloc(sizeof(double) * (ni > 0 ? ni : 1) * ovmax * TR) : NULL;
+    double *ovB = err_ov ? (double *)malloc(sizeof(double) * (ni > 0 ? ni : 1) * ovmax * TR) : NULL;
 
     const int etype = (kind == KIND_ROBIN) ? END_ROBIN : END_DIRICHLET;
     for (int k = 1; k <= K; ++k) {
@@ -496,16 +503,24 @@ static int swr_impl(const orc_problem *P, int kind, double p, double q, int over
             const double *gL = (s > 0) ? (gauss_seidel ? toR_out : toR_in) + (size_t)(s - 1) * TR : NULL;
             const double *gR = (s < S - 1) ? toL_in + (size_t)s * TR : NULL;
             int sendL = (s > 0) ? hi[s - 1] : -1, sendR = (s < S - 1) ? lo[s + 1] : -1;
-            int nrec = 0, rn[2];
+            int nrec = 0;
+            int *rn = (int *)malloc(sizeof(int) * (2 + 2 * (size_t)ovmax));
             int32_t lidx[2];
             if (s > 0) { rn[nrec] = lo[s]; lidx[nrec++] = lo[s]; }
             if (s < S - 1) { rn[nrec] = hi[s]; lidx[nrec++] = hi[s]; }
+            const int nif = nrec, cntL = (err_ov && s > 0) ? hi[s - 1] - lo[s] + 1 : 0,
+                      cntR = (err_ov && s < S - 1) ? hi[s] - lo[s + 1] + 1 : 0;
+            for (int r = 0; r < cntL; ++r) rn[nrec++] = lo[s] + r;      /* shared with s-1 */
+            for (int r = 0; r < cntR; ++r) rn[nrec++] = lo[s + 1] + r;  /* shared with s+1 */
             double *us = slabs + off;
             window(P, lo[s], hi[s], lt, rt, q, p, gL, gR, kind,
                    sendL, (s > 0) ? toL_out + (size_t)(s - 1) * TR : NULL,
                    sendR, (s < S - 1) ? toR_out + (size_t)s * TR : NULL, nrec, rn, rec, us);
+            free(rn);
+            if (cntL) memcpy(ovB + (size_t)(s - 1) * ovmax * TR, rec + (size_t)nif * TR, sizeof(double) * cntL * TR);
+            if (cntR) memcpy(ovA + (size_t)s * ovmax * TR, rec + (size_t)(nif + cntL) * TR, sizeof(double) * cntR * TR);
             /* interface error (all steps n = 1..nt) */
-            for (int i = 0; i < nrec; ++i) {
+            for (int i = 0; i < nif; ++i) {
                 int li = -1;
                 for (int q = 0; q < nl; ++q) if (lines[q] == lidx[i]) { li = q; break; }
                 const double *Ul = Ulines + (size_t)li * TR, *ul = rec + (size_t)i * TR;
@@ -521,6 +536,15 @@ static int swr_impl(const orc_problem *P, int kind, double p, double q, int over
         }
         err_T[k - 1] = eT;
         err_if[k - 1] = eI;
+        if (err_ov) { /* max over the closed overlaps, steps and x-nodes of |u_s - u_{s+1}| */
+            double eo = 0.0;
+            for (int i = 0; i < ni; ++i) {
+                const size_t cnt = (size_t)(hi[i] - lo[i + 1] + 1) * TR;
+                const double *a = ovA + (size_t)i * ovmax * TR, *b = ovB + (size_t)i * ovmax * TR;
+                for (size_t t = 0; t < cnt; ++t) { double d = fabs(a[t] - b[t]); if (d > eo) eo = d; }
+            }
+            err_ov[k - 1] = eo;
+        }
         /* Jacobi exchange: iteration k's outgoing traces feed iteration k+1. */
         double *t;
         t = toL_in; toL_in = toL_out; toL_out = t;
@@ -543,25 +567,28 @@ static int swr_impl(const orc_problem *P, int kind, double p, double q, int over
         }
     }
     free(lo); free(hi); free(lines); free(Ulines); free(Ut);
-    free(toL_in); free(toR_in); free(toL_out); free(toR_out); free(slabs); free(rec);
+    free(toL_in); free(toR_in); free(toL_out); free(toR_out); free(slabs); free(rec); free(ovA); free(ovB);
     return 0;
 }
 int orc_swr_pq(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K,
                double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
-    return swr_impl(P, kind, p, q, overlap, n_sub, K, 0, NULL, NULL, uT_sub, uT, UT, err_T, err_if, traces);
+    return swr_impl(P, kind, p, q, overlap, n_sub, K, 0, NULL, NULL, uT_sub, uT, UT, err_T, err_if, traces, NULL);
 }
 /* Gauss-Seidel schedule (the paper's serial SWR1-SWR4, subdomains in increasing v). */
 int orc_swr_gs(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K,
                double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
-    return swr_impl(P, kind, p, q, overlap, n_sub, K, 1, NULL, NULL, uT_sub, uT, UT, err_T, err_if, traces);
+    return swr_impl(P, kind, p, q, overlap, n_sub, K, 1, NULL, NULL, uT_sub, uT, UT, err_T, err_if, traces, NULL);
 }
 /* General form: schedule (0 Jacobi, 1 Gauss-Seidel) and initial traces init_toL / init_toR
- * ([n_sub-1][nt][nx]: toward the left subdomain's right end / the right subdomain's left end; NULL = 0). */
+ * ([n_sub-1][nt][nx]: toward the left subdomain's right end / the right subdomain's left end; NULL = 0);
+ * err_ov[k-1] (may be NULL): the paper's convergence quantity (eq. 'error'), max over every
+ * closed overlap [lo_{s+1}, hi_s], step and x-node of |u_s^k - u_{s+1}^k| (split FEM: of the Step-1
+ * values w, where the transmission conditions act). */
 int orc_swr_ex(const orc_problem *P, int kind, double p, double q, int overlap, int n_sub, int K, int gauss_seidel,
                const double *init_toL, const double *init_toR,
-               double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {
+               double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces, double *err_ov) {
     return swr_impl(P, kind, p, q, overlap, n_sub, K, gauss_seidel, init_toL, init_toR, uT_sub, uT, UT, err_T, err_if,
-                    traces);
+                    traces, err_ov);
 }
 int orc_swr(const orc_problem *P, int kind, double p, int overlap, int n_sub, int K,
             double *uT_sub, double *uT, double *UT, double *err_T, double *err_if, double *traces) {

@@ -342,6 +342,10 @@ struct kfp_problem_s {
     std::vector<SubDev> subs;  // local block
     SubDev *d_subs = nullptr;
     unsigned long long *d_errT = nullptr, *d_errIF = nullptr;
+    unsigned long long *d_errOV = nullptr;  // [n_rep][K_max] overlap differences (the paper's eq. 'error')
+    bool ovrec = false;                     // overlap recording on (kfp_swr_set_overlap_error)
+    int2 *d_pairs = nullptr;                // local interfaces (left, right subdomain index) of every replica
+    int npairs = 0;
     Plan plan;
     double *d_blkagg = nullptr, *d_chkagg = nullptr, *d_carry = nullptr;
     FusedData fd;                    // fused-kernel tensor maps and tables of the SWR setup
@@ -378,6 +382,10 @@ void free_swr(kfp_problem pb) {
     if (pb->d_errT) cudaFree(pb->d_errT);
     if (pb->d_errIF) cudaFree(pb->d_errIF);
     pb->d_errT = pb->d_errIF = nullptr;
+    pb->d_errOV = nullptr;  // (in swr_allocs)
+    pb->d_pairs = nullptr;
+    pb->npairs = 0;
+    pb->ovrec = false;
     pb->d_blkagg = pb->d_chkagg = pb->d_carry = nullptr;
     pb->fd = FusedData();
     for (int q = 0; q < 2; ++q) pb->edge_sendL[q] = pb->edge_recvL[q] = pb->edge_sendR[q] = pb->edge_recvR[q] = nullptr;
@@ -1319,6 +1327,9 @@ kfp_status swr_setup_impl(kfp_problem pb, kfp_kind kind, const double *ps, const
 
     pb->kind = kind;
     pb->gauss_seidel = false;
+    pb->ovrec = false;
+    pb->d_pairs = nullptr;
+    pb->npairs = 0;
     pb->n_rep = n_rep;
     pb->p = ps[0];
     pb->q_rob = (kind == KFP_ROBIN) ? qs[0] : ps[0];
@@ -1475,6 +1486,9 @@ kfp_status swr_setup_impl(kfp_problem pb, kfp_kind kind, const double *ps, const
         pb->d_errT = static_cast<unsigned long long *>(q);
         KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max * n_rep));
         pb->d_errIF = static_cast<unsigned long long *>(q);
+        KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max * n_rep));
+        pb->d_errOV = static_cast<unsigned long long *>(q);
+        pb->swr_allocs.push_back(reinterpret_cast<double *>(pb->d_errOV));
     }
     KFP_CUDA(cudaMemcpy(pb->d_subs, pb->subs.data(), sizeof(SubDev) * ntot, cudaMemcpyHostToDevice));
     {
@@ -1557,6 +1571,7 @@ kfp_status kfp_swr_reset(kfp_problem pb) {
     if (pb->edge_recvR[0]) KFP_CUDA(cudaMemsetAsync(pb->edge_recvR[0], 0, TR * sizeof(double), pb->stream));
     KFP_CUDA(cudaMemsetAsync(pb->d_errT, 0, sizeof(unsigned long long) * pb->K_max * pb->n_rep, pb->stream));
     KFP_CUDA(cudaMemsetAsync(pb->d_errIF, 0, sizeof(unsigned long long) * pb->K_max * pb->n_rep, pb->stream));
+    KFP_CUDA(cudaMemsetAsync(pb->d_errOV, 0, sizeof(unsigned long long) * pb->K_max * pb->n_rep, pb->stream));
     pb->k_done = 0;
     return KFP_OK;
 }
@@ -1622,6 +1637,7 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
     P.blkagg = pb->d_blkagg;
     P.chkagg = pb->d_chkagg;
     P.carry = pb->d_carry;
+    P.ovrec = pb->ovrec ? 1 : 0;
     KFP_CUDA(cudaEventRecord(pb->ev[0], pb->stream));
     for (int it = 0; it < n_iter; ++it) {
         const int k = pb->k_done + 1;  // 1-based iteration number
@@ -1661,10 +1677,107 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
             for (const SubDev &sd : pb->subs) rows = std::max(rows, sd.hi - sd.lo + 1);
             if (kfp_status st = launch_fem_finish(pb, P, nloc, rows)) return st;
         }
+        if (pb->ovrec && pb->npairs > 0) {  // max |u_s - u_{s+1}| over every local overlap (eq. 'error')
+            kfp::overlap_diff<<<dim3(64, 1, pb->npairs), 256, 0, pb->stream>>>(pb->d_subs, pb->d_pairs, pb->nt, pb->nx,
+                                                                             pb->d_errOV + (k - 1), pb->K_max);
+            pb->launches += 1;
+            KFP_CUDA(cudaGetLastError());
+        }
         KFP_CUDA(cudaEventRecord(pb->ev[3 + 2 * it], pb->stream));
         pb->k_done = k;
     }
     KFP_CUDA(cudaEventRecord(pb->ev[1], pb->stream));
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_set_overlap_error(kfp_problem pb, int32_t on) {
+    if (!pb || !pb->setup) {
+        set_err("kfp_swr_set_overlap_error: no setup");
+        return KFP_E_STATE;
+    }
+    const Plan &pl = pb->plan;
+    if (on && (!pl.fused || pl.col || pl.window)) {
+        set_err("kfp_swr_set_overlap_error: needs the per-step cluster kernel (plan: %s)", pl.text.c_str());
+        return KFP_E_INVAL;
+    }
+    if (!on || pb->ovrec) {
+        pb->ovrec = on != 0;
+        return KFP_OK;
+    }
+    KFP_CUDA(cudaSetDevice(pb->device));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    const int nloc = pb->s_end - pb->s_begin;
+    const size_t TR = (size_t)pb->nt * pb->nx;
+    std::vector<int2> pairs;
+    for (int r = 0; r < pb->n_rep; ++r)
+        for (int i = 0; i + 1 < nloc; ++i) {  // interface between local subdomains i and i+1 of replica r
+            SubDev &L = pb->subs[(size_t)r * nloc + i], &R = pb->subs[(size_t)r * nloc + i + 1];
+            const int a = R.lo, b = L.hi, cnt = b - a + 1;  // the closed overlap [lo_{s+1}, hi_s]
+            L.ovr0[1] = R.ovr0[0] = a;
+            L.ovn[1] = R.ovn[0] = cnt;
+            if (kfp_status st = swr_alloc(pb, &L.ovb[1], (size_t)cnt * TR)) return st;
+            if (kfp_status st = swr_alloc(pb, &R.ovb[0], (size_t)cnt * TR)) return st;
+            pairs.push_back(make_int2(r * nloc + i, r * nloc + i + 1));
+        }
+    if (!pairs.empty()) {
+        void *q = nullptr;
+        KFP_CUDA(cudaMalloc(&q, sizeof(int2) * pairs.size()));
+        pb->d_pairs = static_cast<int2 *>(q);
+        pb->swr_allocs.push_back(static_cast<double *>(q));
+        KFP_CUDA(cudaMemcpy(pb->d_pairs, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice));
+    }
+    pb->npairs = (int)pairs.size();
+    KFP_CUDA(cudaMemcpy(pb->d_subs, pb->subs.data(), sizeof(SubDev) * pb->subs.size(), cudaMemcpyHostToDevice));
+    pb->ovrec = true;
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_overlap_history(kfp_problem pb, int32_t rep, int32_t cap, int32_t *K_out, double *err_ov) {
+    if (!pb || !pb->setup || rep < 0 || rep >= pb->n_rep) {
+        set_err("kfp_swr_overlap_history: no setup or bad replica");
+        return KFP_E_INVAL;
+    }
+    if (!pb->ovrec || pb->k_done == 0) {
+        set_err("kfp_swr_overlap_history: overlap recording off or no iteration");
+        return KFP_E_STATE;
+    }
+    std::vector<unsigned long long> a(pb->k_done);
+    KFP_CUDA(cudaMemcpyAsync(a.data(), pb->d_errOV + (size_t)rep * pb->K_max, sizeof(unsigned long long) * pb->k_done,
+                             cudaMemcpyDeviceToHost, pb->stream));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    if (K_out) *K_out = pb->k_done;
+    for (int k = 0; k < std::min<int>(cap, pb->k_done); ++k) std::memcpy(&err_ov[k], &a[k], 8);
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_iterate_until(kfp_problem pb, kfp_metric metric, double eps, int32_t k_max, int32_t *k_out) {
+    if (!pb || !pb->setup) {
+        set_err("kfp_swr_iterate_until: no setup");
+        return KFP_E_STATE;
+    }
+    if (metric != KFP_ERR_T && metric != KFP_ERR_IF && metric != KFP_ERR_OVERLAP) {
+        set_err("kfp_swr_iterate_until: unknown metric %d", (int)metric);
+        return KFP_E_INVAL;
+    }
+    if (metric == KFP_ERR_OVERLAP && !pb->ovrec) {
+        set_err("kfp_swr_iterate_until: KFP_ERR_OVERLAP needs kfp_swr_set_overlap_error(pb, 1)");
+        return KFP_E_STATE;
+    }
+    if (k_max < 0 || pb->k_done + k_max > pb->K_max) {
+        set_err("kfp_swr_iterate_until: %d + %d iterations exceed K_max=%d", pb->k_done, k_max, pb->K_max);
+        return KFP_E_STATE;
+    }
+    const unsigned long long *hist = metric == KFP_ERR_T ? pb->d_errT : metric == KFP_ERR_IF ? pb->d_errIF : pb->d_errOV;
+    for (int i = 0; i < k_max; ++i) {
+        if (kfp_status st = kfp_swr_iterate(pb, 1)) return st;
+        unsigned long long bits = 0;  // replica 0 (the batch's first replica)
+        KFP_CUDA(cudaMemcpyAsync(&bits, hist + (pb->k_done - 1), sizeof bits, cudaMemcpyDeviceToHost, pb->stream));
+        KFP_CUDA(cudaStreamSynchronize(pb->stream));
+        double e;
+        std::memcpy(&e, &bits, 8);
+        if (!(e >= eps)) break;  // below the tolerance (or NaN: stop as well)
+    }
+    if (k_out) *k_out = pb->k_done;
     return KFP_OK;
 }
 

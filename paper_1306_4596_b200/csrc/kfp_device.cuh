@@ -60,6 +60,10 @@ struct SubDev {
     const double *gL[2], *gR[2]; // incoming traces [nt][nx] by iteration parity
     double *sendL[2], *sendR[2]; // outgoing traces [nt][nx] by iteration parity
     double tpL, tpR;             // Robin parameter of the trace sent left (p: it lands on a right end) and right (q)
+    // overlap recording (the paper's stopping rule, eq. 'error' P:588-592; opt-in): side 0 = the nodes
+    // [lo_s, hi_{s-1}] shared with s-1, side 1 = [lo_{s+1}, hi_s] shared with s+1; ovn = 0: not recorded
+    int ovr0[2], ovn[2];         // first node, node count
+    double *ovb[2];              // [ovn][nt][nx] this subdomain's values there (u; split FEM: w)
 };
 
 struct StepParams {
@@ -77,6 +81,7 @@ struct StepParams {
     int P, b, R, C;        // warps per CTA, rows per chunk, rows per block, blocks per column
     int qtab_len;
     int record;            // monodomain: record rows listed in line_of_node
+    int ovrec;             // record the overlap rows into SubDev::ovb (cluster kernel only)
     double q, a, qa, hv, dt, p;   // split FEM: a = tau/h_v^2 - 1/6, dt = tau
     double dnu, nu0;       // split FEM transport weight of node j: |j dnu + nu0| = |v_j| tau / h_x (0 at n = 0)
     double cf[kMaxRank];   // dt * ft[r][n+1]

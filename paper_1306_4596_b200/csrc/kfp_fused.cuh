@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
     bool chunk_special = false;
 #pragma unroll
     for (int qq = 0; qq < 6; ++qq) chunk_special |= sp_row[qq] >= cr0 && sp_row[qq] < cr0 + Lw;
-    bool cta_special = trace_cta || P.record;
+    bool cta_special = trace_cta || P.record || P.ovrec;
 #pragma unroll
     for (int qq = 4; qq < 6; ++qq) cta_special |= inblk(sp_row[qq]);
     const int t_first = blockIdx.y;
@@ -697,6 +697,18 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                         if (inblk(row))
                             P.rec[(static_cast<size_t>(i) * P.nt + P.n) * P.nx + m] = unew[static_cast<size_t>(row) * P.nx + m];
                     }
+                if (P.ovrec)  // this subdomain's overlap rows (unknown rows of this block; Dirichlet end nodes)
+                    for (int side = 0; side < 2; ++side)
+                        for (int r = 0; r < S.ovn[side]; ++r) {
+                            const int node = S.ovr0[side] + r, row = node - S.first;
+                            double val = 0.0;
+                            bool have = true;
+                            if (row >= 0 && row < n && inblk(row)) val = unew[static_cast<size_t>(row) * P.nx + m];
+                            else if (node == S.lo && S.ltype == END_DIRI && blk == 0) val = sm.gin[lane];
+                            else if (node == S.hi && S.rtype == END_DIRI && blk == nblk - 1) val = sm.gin[kWarp + lane];
+                            else have = false;
+                            if (have) S.ovb[side][(static_cast<size_t>(r) * P.nt + P.n) * P.nx + m] = val;
+                        }
             }
         }
         KFP_TT(5)
@@ -757,6 +769,29 @@ __global__ void __launch_bounds__(128) fem_finish(const StepParams P) {
             e = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
             if (e > 0.0) atomic_max_pos(P.errT + static_cast<size_t>(S.grp) * P.err_stride, e);
         }
+    }
+}
+
+// The paper's stopping quantity (eq. 'error'): max over the closed overlap of interface z
+// (nodes [lo_{s+1}, hi_s]), every step and x-node of |u_s - u_{s+1}|, from the two subdomains' overlap
+// records; one atomic max per CTA into errOV + grp * err_stride.  grid (blocks, 1, interfaces).
+__global__ void __launch_bounds__(256) overlap_diff(const SubDev *subs, const int2 *pairs, int nt, int nx,
+                                                    unsigned long long *errOV, int err_stride) {
+    const int2 pr = pairs[blockIdx.z];
+    const SubDev &L = subs[pr.x], &R = subs[pr.y];
+    const size_t N = static_cast<size_t>(L.ovn[1]) * nt * nx;
+    const double *a = L.ovb[1], *b = R.ovb[0];
+    double e = 0.0;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        e = fmax(e, fabs(a[i] - b[i]));
+    __shared__ double red[8];
+    e = warp_max(e);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) e = fmax(e, red[w]);
+        if (e > 0.0) atomic_max_pos(errOV + static_cast<size_t>(L.grp) * err_stride, e);
     }
 }
 

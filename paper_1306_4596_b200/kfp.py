@@ -17,7 +17,8 @@ LIB_PATH = os.environ.get("KFP_LIB_PATH") or os.path.join(_HERE, "libkfp.so")  #
 
 KFP_OK, KFP_E_INVAL, KFP_E_CFL, KFP_E_NOMEM, KFP_E_CUDA, KFP_E_STATE = 0, -1, -2, -3, -4, -6
 KIND = {"dirichlet": 0, "robin": 1}
-SCHEME = {"imex_fd": 0, "split_fem": 1}  # kfp_scheme (include/kfp.h)
+SCHEME = {"imex_fd": 0, "split_fem": 1}
+METRIC = {"err_T": 0, "err_if": 1, "overlap": 2}  # kfp_metric  # kfp_scheme (include/kfp.h)
 
 # Every symbol include/kfp.h declares (checked by tests/test_abi.py).
 SYMBOLS = (
@@ -26,6 +27,7 @@ SYMBOLS = (
     "kfp_swr_reset", "kfp_swr_iterate", "kfp_swr_edge_buffers", "kfp_swr_bind_edge_buffers", "kfp_swr_solve", "kfp_error_history",
     "kfp_swr_subdomain_uT", "kfp_swr_subdomain_range", "kfp_swr_trace", "kfp_monodomain_uT", "kfp_launch_count",
     "kfp_plan", "kfp_last_timing", "kfp_last_error",
+    "kfp_swr_set_overlap_error", "kfp_swr_overlap_history", "kfp_swr_iterate_until",
 )
 
 
@@ -90,6 +92,9 @@ def load(path: str = LIB_PATH):
         "kfp_plan": (ctypes.c_char_p, [vp]),
         "kfp_last_timing": (i32, [vp, pd, pd]),
         "kfp_last_error": (ctypes.c_char_p, []),
+        "kfp_swr_set_overlap_error": (i32, [vp, i32]),
+        "kfp_swr_overlap_history": (i32, [vp, i32, i32, ctypes.POINTER(i32), vp]),
+        "kfp_swr_iterate_until": (i32, [vp, i32, dbl, i32, ctypes.POINTER(i32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -261,6 +266,24 @@ class Problem:
         out = np.empty((g.nt, g.nx))
         _check(load().kfp_swr_trace(self._h, int(i), int(direction), _ptr(out)))
         return out
+
+    def set_overlap_error(self, on: bool = True):
+        """Record the paper's convergence quantity max |u_s - u_{s+1}| over the overlaps."""
+        _check(load().kfp_swr_set_overlap_error(self._h, 1 if on else 0))
+
+    def overlap_history(self, rep: int = 0):
+        k = ctypes.c_int32(0)
+        cap = 1 << 16
+        out = np.zeros(cap)
+        _check(load().kfp_swr_overlap_history(self._h, rep, cap, ctypes.byref(k), _ptr(out)))
+        return out[: k.value].copy()
+
+    def iterate_until(self, eps: float, k_max: int, metric: str = "overlap") -> int:
+        """Iterate until the chosen error of the last iteration is below eps (or k_max more iterations);
+        returns the iterations done since the last reset."""
+        k = ctypes.c_int32(0)
+        _check(load().kfp_swr_iterate_until(self._h, METRIC[metric], float(eps), int(k_max), ctypes.byref(k)))
+        return int(k.value)
 
     def launch_count(self) -> int:
         return int(load().kfp_launch_count(self._h))

@@ -190,3 +190,24 @@ def test_fem_reproduces_paper_table1_level0(orc):
     # trace, so u1 - u2 vanishes identically; the iterates themselves do not approach the solution 0
     _, _, size = _paper_table1(orc, 0, 0, "dirichlet", 0.0, None, kmax=25, eps=0.0)
     assert size[-1] > 0.5 * size[9] > 1e-3
+
+
+@pytest.mark.parametrize("kind,p,q,ov", [("robin", 11.0, 2.5, 3), ("robin", 4.23, None, 0), ("dirichlet", 0.0, None, 3)])
+def test_overlap_error_matches_direct_loop(orc, kind, p, q, ov):
+    """err_ov of the oracle's SWR driver (Gauss-Seidel, random lambda_1^0) == the paper's quantity computed
+    directly from SWR1-SWR4 window by window (eq. 'error')."""
+    g = ki.Grid(50, 100, 40, 1.0, 0.4)
+    seed = 77
+    lam1 = np.random.default_rng(seed).uniform(-1.0, 1.0, size=(g.nt, g.nx))
+    prob = ki.fem_problem(g)
+    r = orc.swr(prob, kind, p, ov, 2, 5, q=q, schedule="gauss_seidel",
+                init_traces=(lam1[None], np.zeros((1, g.nt, g.nx))))
+    lo, hi = orc.subdomains(g.nv, 2, ov)
+    et = END_ROBIN if kind == "robin" else END_DIRICHLET
+    alpha, beta = int(lo[1]), int(hi[0])
+    nodes = list(range(alpha, beta + 1))
+    lam = lam1
+    for k in range(5):
+        _, _, lam2, r1 = orc.window(prob, 0, beta, END_PHYS, et, p, None, lam, kind, -1, alpha, nodes, q=q)
+        _, lam, _, r2 = orc.window(prob, alpha, g.nv, et, END_PHYS, p, lam2, None, kind, beta, -1, nodes, q=q)
+        assert abs(r["err_ov"][k] - np.abs(r1 - r2).max()) <= 1e-14 * max(1.0, r["err_ov"][0]), k

@@ -154,3 +154,69 @@ def test_fem_batched_sweep_equals_individual(kfp):
         assert np.array_equal(eT, hist[0]) and np.array_equal(eI, hist[1]), r
         for a, b in zip(bs, slabs):
             assert np.array_equal(a, b), r
+
+
+@pytest.mark.parametrize("name", ["robin_S2", "robin_pq_S3_ragged_ov1", "dirichlet_ov3", "robin_ov3_S4",
+                                  "gs_robin_pq", "lam_dirichlet_gs", "paper_j0"])
+def test_overlap_error_vs_oracle(kfp, name):
+    """The paper's convergence quantity max |u_s - u_{s+1}| over the closed overlaps (eq. 'error'),
+    recorded by the cluster kernel and reduced on the device, against the oracle's."""
+    c = CASES[name]
+    prob = ki.fem_problem(c.grid, c.seed)
+    with kfp.Problem(prob) as pb:
+        pb.setup(c.kind, c.p, c.ov, c.S, c.K, q=c.q)
+        pb.set_schedule(c.schedule)
+        pb.set_overlap_error(True)
+        pb.reset()
+        if c.lam:
+            toL, toR = _lam(c)
+            for i in range(c.S - 1):
+                pb.set_initial_trace(i, 0, toL[i])
+                pb.set_initial_trace(i, 1, toR[i])
+        pb.iterate(c.K)
+        eo = pb.overlap_history()
+        eT, eI = pb.history()
+    r = _oracle(name)
+    assert rel(eo, r["err_ov"]) <= TOL, (name, eo, r["err_ov"])
+    assert rel(eT, r["err_T"]) <= TOL and rel(eI, r["err_if"]) <= TOL  # the recording changes nothing else
+
+
+def test_overlap_error_imex_fd(kfp):
+    """The same quantity for the IMEX FD scheme (Dirichlet end nodes of CSWR included)."""
+    import oracle
+
+    run = ki.scaled(ki.config("c1"), nx=40, nt=100, K=5, name="ov_fd").with_(n_sub=4, overlap=6)
+    prob = ki.make_problem(run)
+    with kfp.Problem(prob) as pb:
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        pb.set_overlap_error(True)
+        pb.reset()
+        pb.iterate(run.K)
+        eo = pb.overlap_history()
+    r = oracle.swr(prob, run.kind, run.p, run.overlap, run.n_sub, run.K)
+    assert rel(eo, r["err_ov"]) <= TOL, (eo, r["err_ov"])
+
+
+def test_iterate_until_tolerance(kfp):
+    """Tolerance stopping: kfp_swr_iterate_until stops at the first iteration whose overlap error is
+    below eps -- the same k the oracle's history gives."""
+    import oracle
+
+    c = CASES["paper_j0"]
+    prob = ki.fem_problem(c.grid, c.seed)
+    toL, toR = _lam(c)
+    r = oracle.swr(prob, c.kind, c.p, c.ov, c.S, 20, q=c.q, schedule=c.schedule, init_traces=(toL, toR))
+    eps = 1e-6
+    k_ref = int(np.nonzero(r["err_ov"] < eps)[0][0]) + 1
+    with kfp.Problem(prob) as pb:
+        pb.setup(c.kind, c.p, c.ov, c.S, 20, q=c.q)
+        pb.set_schedule(c.schedule)
+        pb.set_overlap_error(True)
+        pb.reset()
+        for i in range(c.S - 1):
+            pb.set_initial_trace(i, 0, toL[i])
+            pb.set_initial_trace(i, 1, toR[i])
+        k = pb.iterate_until(eps, 20)
+        eo = pb.overlap_history()
+    assert k == k_ref, (k, k_ref, r["err_ov"])
+    assert rel(eo, r["err_ov"][:k]) <= TOL
