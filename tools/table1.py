@@ -1,14 +1,21 @@
-"""The paper's Table 1 experiment re-run with this library's discretisation on one B200.
+"""The paper's Table 1 experiment re-run on one B200, with either discretisation.
 
-Error equation (f = 0, u0 = 0) on x in [0,1) periodic, v in [-1,1] (Dirichlet 0 ends; the paper uses Neumann and
-notes the end condition does not matter), T = 2, Delta t = h_x = h_v = 0.01 / 2^j (j = 0..4), two
-subdomains split at v = 0 with overlap 3 h_v or none, random initial traces lambda^0 ~ U(-1, 1), the
-paper's serial schedule SWR1-SWR4 (Gauss-Seidel), stop when the interface error drops below
-eps = 1e-6 (our err_if: max over interface nodes and time of |u_s^k| -- the exact solution is 0) or after 150
-iterations.  Robin parameters as in the paper: OSWR(p) p = 4.23, OSWR(p, q) p = 11, q = 2.5.
+--scheme fem (default; the paper's own): split FEM, Neumann ends, tau = dt/2, and the
+paper's stopping rule: max over the closed overlap, t and x of |u1 - u2| < eps (eq. 'error'),
+recorded and reduced on the GPU (kfp_swr_set_overlap_error / kfp_swr_iterate_until).  Without overlap the
+classical method's overlap is the single interface node where both Dirichlet values are the same trace
+(|u1 - u2| = 0 identically), so CSWR ov=0 is judged by err_if (the iterates against the exact solution 0).
+--scheme fd: this library's IMEX FD scheme (Dirichlet 0 ends), stopping on err_if.
 
-    python tools/table1.py [jmax] > profiles/r1_table1.json
+Common: error equation f = 0, u0 = 0 on x in [0,1) periodic, v in [-1,1], T = 2,
+Delta t = h_x = h_v = 0.01 / 2^j (j = 0..4), two subdomains split at v = 0 with overlap 3 h_v or none, random
+lambda_1^0 ~ U(-1, 1), the paper's serial schedule SWR1-SWR4 (Gauss-Seidel), eps = 1e-6,
+at most 150 iterations; OSWR(p) p = 4.23, OSWR(p, q) p = 11, q = 2.5.
+
+    python tools/table1.py [--scheme fem|fd] [--jmax 4] > profiles/r1_table1_fem.json
 """
+import argparse
+import dataclasses
 import json
 import os
 import sys
@@ -28,44 +35,61 @@ PAPER = {  # Table 1 of the paper (its own FEM discretisation), for context only
 METHODS = [("CSWR", "dirichlet", 0.0, None), ("OSWR(p)", "robin", 4.23, None), ("OSWR(p,q)", "robin", 11.0, 2.5)]
 
 
-def run_level(j, ov, name, kind, p, q):
-    g = ki.Grid(100 * 2 ** j, 200 * 2 ** j, 200 * 2 ** j, 1.0, 2.0)
-    prob = ki.zero_problem(g)
+def run_level(j, ov, name, kind, p, q, scheme, tau_full=False, lam_lo=-1.0):
+    g = ki.paper_grid(j)
+    fem = scheme == "fem"
+    if fem and tau_full:  # reading-F2 alternative: both sub-steps over Delta t (T doubled, same step count)
+        g = dataclasses.replace(g, t_final=2.0 * g.t_final)
+    prob = ki.fem_problem(g) if fem else ki.zero_problem(g)
     rng = np.random.default_rng(1000 + j)
-    lam = [rng.uniform(-1.0, 1.0, size=(g.nt, g.nx)) for _ in range(2)]
-    hist = []
+    lam = [rng.uniform(lam_lo, 1.0, size=(g.nt, g.nx)) for _ in range(2)]
+    metric = "overlap" if fem and not (kind == "dirichlet" and ov == 0) else "err_if"
     t0 = time.perf_counter()
     with Problem(prob) as pb:
         pb.setup(kind, p if kind == "robin" else 0.0, ov, 2, KMAX, q=q)
         pb.set_schedule("gauss_seidel")
+        if metric == "overlap":
+            pb.set_overlap_error(True)
         pb.reset()
         pb.set_initial_trace(0, 0, lam[0])  # lambda_1^0 (toward Omega_1's right end)
         pb.set_initial_trace(0, 1, lam[1])  # unused by SWR1-SWR4 (lambda_2^k comes from u_1^k)
-        it = None
-        for k in range(1, KMAX + 1):
-            pb.iterate(1)
-            e = float(pb.history()[1][-1])
-            hist.append(e)
-            if e < EPS:
-                it = k
-                break
-            if not np.isfinite(e) or (k >= 30 and e > 0.999 * hist[k - 30]):
-                break  # no progress (CSWR without overlap)
-    return dict(grid=[g.nx, g.nv, g.nt], iterations=it if it is not None else (f">{KMAX}" if len(hist) == KMAX else "-"),
-                err_if=hist, seconds=time.perf_counter() - t0)
+        if metric == "overlap":
+            k = pb.iterate_until(EPS, KMAX, "overlap")
+            hist = list(pb.overlap_history())
+        else:  # stall detection for the non-converging classical method
+            hist = []
+            for k in range(1, KMAX + 1):
+                pb.iterate(1)
+                hist.append(float(pb.history()[1][-1]))
+                if hist[-1] < EPS or (k >= 30 and hist[-1] > 0.999 * hist[k - 30]):
+                    break
+        secs = time.perf_counter() - t0
+        plan = pb.plan()
+    it = len(hist)
+    conv = hist[-1] < EPS
+    label = it if conv else (f">{KMAX}" if it == KMAX else "-")
+    return dict(grid=[g.nx, g.nv, g.nt], iterations=label, metric=metric, history=hist, seconds=secs, plan=plan,
+                updates=g.nx * g.nv * g.nt * it)
 
 
 def main():
-    jmax = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-    out = {"eps": EPS, "kmax": KMAX, "schedule": "gauss_seidel (SWR1-SWR4)", "results": {}}
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scheme", choices=["fem", "fd"], default="fem")
+    ap.add_argument("--jmax", type=int, default=4)
+    ap.add_argument("--tau-full", action="store_true", help="FEM: tau = Delta t instead of Delta t / 2 (reading F2)")
+    ap.add_argument("--lam-unit", action="store_true", help="lambda^0 ~ U(0, 1) instead of U(-1, 1)")
+    a = ap.parse_args()
+    out = {"scheme": {"fem": "split_fem (the paper's, P:443-525)", "fd": "imex_fd"}[a.scheme], "eps": EPS,
+           "kmax": KMAX, "schedule": "gauss_seidel (SWR1-SWR4)", "tau": "dt" if a.tau_full else "dt/2",
+           "lambda0": "U(0,1)" if a.lam_unit else "U(-1,1)", "results": {}}
     for ov in (3, 0):
         for name, kind, p, q in METHODS:
             row = []
-            for j in range(jmax + 1):
-                r = run_level(j, ov, name, kind, p, q)
+            for j in range(a.jmax + 1):
+                r = run_level(j, ov, name, kind, p, q, a.scheme, a.tau_full, 0.0 if a.lam_unit else -1.0)
                 row.append(r)
-                print(f"ov={ov} {name:10s} j={j} iterations={r['iterations']} ({r['seconds']:.1f} s)", file=sys.stderr,
-                      flush=True)
+                print(f"{a.scheme} ov={ov} {name:10s} j={j} iterations={r['iterations']} ({r['seconds']:.1f} s)",
+                      file=sys.stderr, flush=True)
             out["results"][f"{name} ov={ov}"] = {"ours": [r["iterations"] for r in row],
                                                  "paper": PAPER[(name, ov)], "levels": row}
     print(json.dumps(out))
