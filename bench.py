@@ -128,7 +128,7 @@ def run_cpu_oracle(run: ki.Run, steps: int = 1):
     updates = g.nx * g.nv * g.nt * (1 + sample.K)  # monodomain window + K iterations of windows
     t0 = time.perf_counter()
     for _ in range(steps):
-        oracle.swr(prob, sample.kind, sample.p, sample.overlap, sample.n_sub, sample.K)
+        oracle.swr(prob, sample.kind, sample.p, sample.overlap, sample.n_sub, sample.K, q=sample.q)
     dt = time.perf_counter() - t0
     text = (f"{run.name} grid {g.nx}x{g.nv}, same dt/CFL, window cut to n_t={g.nt} steps, K=1, "
             f"plus the monodomain window; {updates:.3g} updates per step")
@@ -168,7 +168,7 @@ def bench_single(args):
     stream = torch.cuda.current_stream()
     pb = Problem(prob, device=dev)
     pb.set_stream(stream.cuda_stream)
-    pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)  # monodomain reference happens here (untimed)
+    pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)  # monodomain reference here (untimed)
     torch.cuda.synchronize()
 
     def one():
@@ -200,7 +200,9 @@ def bench_single(args):
 
     # roofline of the dominant kernel (the fused step): algorithmic bytes per launch / avg duration
     rows = sum(pb.subdomain_range(s)[1] - pb.subdomain_range(s)[0] + 1 for s in range(run.n_sub))
-    unknown_rows = rows - 2 * (run.n_sub - 1) * (0 if run.kind == "robin" else 1) - 2  # physical ends not solved
+    # Dirichlet interface ends and (IMEX FD) the physical ends are not solved; the split-FEM scheme's
+    # physical ends are Neumann (unknown)
+    unknown_rows = rows - 2 * (run.n_sub - 1) * (0 if run.kind == "robin" else 1) - (0 if run.scheme == "split_fem" else 2)
     step_launches = g.nt * run.K * args.steps
     per_launch_s = step_kernel_ms / 1e3 / step_launches
     bytes_per_launch = BYTES_PER_UPDATE * g.nx * unknown_rows
@@ -218,7 +220,7 @@ def bench_single(args):
     for _ in range(e2e_steps):
         with Problem(prob, device=dev) as q:
             q.set_stream(stream.cuda_stream)
-            uT = q.solve(run.kind, run.p, run.overlap, run.n_sub, run.K)
+            uT = q.solve(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
             h = q.history()
             d2h = uT.nbytes + h[0].nbytes + h[1].nbytes
     e1.record(stream)
@@ -236,7 +238,7 @@ def bench_single(args):
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": run.name, "nx": g.nx, "nv": g.nv, "nt": g.nt, "K": run.K, "n_sub": run.n_sub,
-                   "kind": run.kind, "p": run.p, "overlap": run.overlap, "plan": plan,
+                   "kind": run.kind, "p": run.p, "q": run.q, "overlap": run.overlap, "scheme": run.scheme, "plan": plan,
                    "l2": "inputs larger than L2 (two fp64 slab pairs of %.0f MB vs 126 MB L2)" %
                          (2 * 8 * g.nx * (g.nv + run.n_sub) / 1e6),
                    "parallelism": "v-subdomains on 1 GPU", "updates_per_step": updates},

@@ -117,6 +117,7 @@ class Run:
     n_sub: int
     K: int
     q: Optional[float] = None  # two-sided OSWR(p, q): Robin parameter of the left ends (None: q = p)
+    scheme: str = "imex_fd"    # discretisation (SCHEMES)
 
     @property
     def updates(self) -> int:
@@ -203,6 +204,8 @@ def paper_grid(j: int) -> Grid:
 
 
 def make_problem(run: Run) -> Problem:
+    if run.scheme == "split_fem":
+        return fem_problem(run.grid, u0_seed=0 if run.data == "random_u0" else None)
     if run.data == "mms":
         return mms_problem(run.grid)
     if run.data == "random":
@@ -219,6 +222,10 @@ CONFIGS = {
     "c2": Run("c2", Grid(4096, 4096, 1000, 4.0, 0.05), "mms", "robin", 4.0, 0, 2, 10),
     "c3": Run("c3", Grid(8192, 16384, 1000, 4.0, 0.02), "mms", "robin", 8.0, 0, 8, 15),
     "c4": Run("c4", Grid(2048, 32768, 500, 4.0, 0.01), "random", "dirichlet", 0.0, 4, 32, 30),
+    # not a BASELINE.json config: the paper's finest Table 1 mesh with its own split-FEM scheme,
+    # OSWR(11, 2.5) with overlap 3 h_v, Jacobi, random rank-2 u0 (a bench workload for that kernel)
+    "paper_j4": Run("paper_j4", Grid(1600, 3200, 3200, 1.0, 2.0), "random_u0", "robin", 11.0, 3, 2, 10, q=2.5,
+                    scheme="split_fem"),
 }
 
 
