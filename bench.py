@@ -165,7 +165,10 @@ def bench_single(args):
     prob = ki.make_problem(run)
     dev = 0
     torch.cuda.set_device(dev)
-    stream = torch.cuda.current_stream()
+    # a real stream (not the legacy default, handle 0, which kfp_set_stream reads as "the library's own
+    # stream"): the library launches on it and the timing events are recorded on it
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     pb = Problem(prob, device=dev)
     pb.set_stream(stream.cuda_stream)
     pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)  # monodomain reference here (untimed)
@@ -258,7 +261,18 @@ def bench_single(args):
     return 0
 
 
+def _json_stdout():
+    """Keep stdout for the one JSON line: native code (NCCL's banner and messages, any printf) writes to file
+    descriptor 1, so fd 1 is pointed at stderr and the JSON line goes to a duplicate of the original stdout."""
+    sys.stdout.flush()
+    out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    sys.stdout = out
+    return out
+
+
 def main():
+    _json_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)

@@ -244,6 +244,17 @@ kfp_status kfp_swr_set_overlap_error(kfp_problem pb, int32_t on);
  * recording is off or no iteration ran. */
 kfp_status kfp_swr_overlap_history(kfp_problem pb, int32_t rep, int32_t cap, int32_t *K_out, double *err_ov);
 
+/* Pipelined Jacobi iterations (the Remark P:594-597): iteration k+1's step n needs
+ * only trace row n of iteration k, so one sweep of nt + depth - 1 launches advances `depth` consecutive
+ * iterations, slot d running iteration k0 + d at step L - d in launch L.  Results are identical to the
+ * unpipelined schedule (bitwise: same per-tile arithmetic); latency-bound small problems gain up to
+ * depth x parallelism per launch.  Allocates (depth - 1) extra slabs per subdomain and depth + 1 trace
+ * buffers per interface and direction.  depth >= 2 needs a fresh setup (call right after setup /
+ * reset), the Jacobi schedule, every subdomain on this process, the per-step cluster kernel and no
+ * overlap recording -> else KFP_E_INVAL / KFP_E_STATE.  kfp_swr_iterate then runs in groups of <= depth
+ * iterations (one host synchronisation per group); kfp_last_timing reports per-group windows. */
+kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth);
+
 /* Tolerance stopping: run single iterations until `metric` of the last one (replica 0) is
  * below eps (or not finite), or k_max more iterations have run; *k_out = iterations done since the last
  * reset.  Each iteration synchronises the stream once to read its error (8 bytes).  KFP_E_STATE if

@@ -77,22 +77,26 @@ struct FusedData {
 };
 
 using FusedKernel = void (*)(const kfp::FusedParams);
-template <int B, int NR, int P, bool FEM = false>
+template <int B, int NR, int P, bool FEM = false, bool PIPE = false>
 void fused_entry(FusedKernel *k, size_t *smem) {
-    *k = kfp::step_fused_tma<B, NR, P, FEM>;
+    *k = kfp::step_fused_tma<B, NR, P, FEM, PIPE>;
     *smem = kfp::fused_smem_bytes<B, NR, P, FEM>();
 }
-// instantiated (B, NR, P) combinations of the fused kernel; the split-FEM scheme (no forcing) uses NR = 2
-bool fused_kernel(int B, int NR, int P, FusedKernel *k, size_t *smem, bool fem = false) {
-#define KFP_ENTRY(BB, NN, PP)                        \
-    if (!fem && B == BB && NR == NN && P == PP) {    \
-        fused_entry<BB, NN, PP>(k, smem);            \
-        return true;                                 \
+// instantiated (B, NR, P) combinations of the fused kernel; the split-FEM scheme (no forcing) uses NR = 2;
+// pipelined-iteration variants (pipe) exist for NR = 2
+bool fused_kernel(int B, int NR, int P, FusedKernel *k, size_t *smem, bool fem = false, bool pipe = false) {
+#define KFP_ENTRY(BB, NN, PP)                                    \
+    if (!fem && B == BB && NR == NN && P == PP) {                \
+        if (!pipe) fused_entry<BB, NN, PP>(k, smem);             \
+        else if (NN == 2) fused_entry<BB, 2, PP, false, true>(k, smem); \
+        else return false;                                       \
+        return true;                                             \
     }
-#define KFP_FENTRY(BB, PP)                           \
-    if (fem && B == BB && NR == 2 && P == PP) {      \
-        fused_entry<BB, 2, PP, true>(k, smem);       \
-        return true;                                 \
+#define KFP_FENTRY(BB, PP)                                       \
+    if (fem && B == BB && NR == 2 && P == PP) {                  \
+        if (!pipe) fused_entry<BB, 2, PP, true>(k, smem);        \
+        else fused_entry<BB, 2, PP, true, true>(k, smem);        \
+        return true;                                             \
     }
     KFP_ENTRY(8, 2, 8) KFP_ENTRY(16, 2, 8) KFP_ENTRY(17, 2, 8) KFP_ENTRY(32, 2, 8) KFP_ENTRY(33, 2, 8)
     KFP_ENTRY(8, 4, 8) KFP_ENTRY(16, 4, 8) KFP_ENTRY(17, 4, 8) KFP_ENTRY(32, 4, 8) KFP_ENTRY(33, 4, 8)
@@ -319,6 +323,7 @@ struct kfp_problem_s {
     std::vector<double> fv_host;  // host [f_rank][nv+1]
     double *d_fv = nullptr, *d_fx = nullptr, *d_u0v = nullptr, *d_u0x = nullptr;
     double2 *d_rowc = nullptr;
+    double *d_cfn = nullptr;  // [nt][kMaxRank] dt * ft[r][n+1] (the cluster kernel's per-step forcing weights)
     double *d_qp = nullptr, *d_s2 = nullptr;
     int qtab_len = 0;
     std::vector<void *> allocs;  // everything else (freed at destroy)
@@ -346,6 +351,14 @@ struct kfp_problem_s {
     bool ovrec = false;                     // overlap recording on (kfp_swr_set_overlap_error)
     int2 *d_pairs = nullptr;                // local interfaces (left, right subdomain index) of every replica
     int npairs = 0;
+    // pipelined Jacobi iterations (kfp_swr_set_pipeline): depth D, D slots of every descriptor (slot d
+    // runs iteration k0 + d, lagging d steps), trace rings of D + 1 buffers per interface and direction
+    int pipe = 1;
+    std::vector<SubDev> psubs;             // [D][ntot], slot-major
+    SubDev *d_psubs = nullptr;
+    FusedData pfd;                         // tensor maps / level-2 maps of psubs (tables shared with fd)
+    std::vector<std::vector<double *>> ringL, ringR;  // [rep * (nloc-1) + i][D+1]: sent left / right
+    std::vector<const double *> final_slab;           // [ntot] u(T) of the last iteration (pipelined)
     Plan plan;
     double *d_blkagg = nullptr, *d_chkagg = nullptr, *d_carry = nullptr;
     FusedData fd;                    // fused-kernel tensor maps and tables of the SWR setup
@@ -386,6 +399,13 @@ void free_swr(kfp_problem pb) {
     pb->d_pairs = nullptr;
     pb->npairs = 0;
     pb->ovrec = false;
+    pb->pipe = 1;
+    pb->psubs.clear();
+    pb->d_psubs = nullptr;  // (in swr_allocs)
+    pb->pfd = FusedData();
+    pb->ringL.clear();
+    pb->ringR.clear();
+    pb->final_slab.clear();
     pb->d_blkagg = pb->d_chkagg = pb->d_carry = nullptr;
     pb->fd = FusedData();
     for (int q = 0; q < 2; ++q) pb->edge_sendL[q] = pb->edge_recvL[q] = pb->edge_sendR[q] = pb->edge_recvR[q] = nullptr;
@@ -505,6 +525,7 @@ StepParams base_params(kfp_problem pb) {
     P.dnu = pb->dnu;
     P.nu0 = pb->nu0;
     P.rowc = pb->d_rowc;
+    P.cfn = pb->d_cfn;
     P.fv = pb->d_fv;
     P.fx = pb->d_fx;
     P.u0v = pb->d_u0v;
@@ -515,14 +536,16 @@ StepParams base_params(kfp_problem pb) {
     return P;
 }
 
-// One time step of every subdomain in P.subs (nsub entries).
+// One time step of every subdomain in P.subs (nsub entries); pipe: the pipelined-iteration variant
+// (each descriptor at step n - lag).
 kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, int n, const FusedData &fd,
-                       int nrec = 0, const int *rec_rows = nullptr) {
+                       int nrec = 0, const int *rec_rows = nullptr, bool pipe = false) {
     P.n = n;
     P.from_u0 = (n == 0);
-    // split FEM: step n transports w^{n-1/2} (the previous step's Step 2) before its Step 1; step 0 starts from u0
-    P.dnu = (n == 0) ? 0.0 : pb->dnu;
-    P.nu0 = (n == 0) ? 0.0 : pb->nu0;
+    // split FEM: step n transports w^{n-1/2} (the previous step's Step 2) before its Step 1; the kernel
+    // drops the transport at step 0 (it starts from u0)
+    P.dnu = pb->dnu;
+    P.nu0 = pb->nu0;
     for (int r = 0; r < kfp::kMaxRank; ++r) P.cf[r] = (r < pb->f_rank) ? pb->dt * pb->ft[(size_t)r * (pb->nt + 1) + n + 1] : 0.0;
     P.P = pl.P;
     P.b = pl.b;
@@ -579,7 +602,10 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
         FP.tabs = fd.tabs;
         FusedKernel k;
         size_t smem;
-        fused_kernel(pl.B, pl.NR, pl.P, &k, &smem, pl.fem);
+        if (!fused_kernel(pl.B, pl.NR, pl.P, &k, &smem, pl.fem, pipe)) {
+            set_err("launch_step: no fused kernel for B=%d NR=%d P=%d%s", pl.B, pl.NR, pl.P, pipe ? " (pipelined)" : "");
+            return KFP_E_INVAL;
+        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(pl.C, FP.Gc, nsub);
         cfg.blockDim = block;
@@ -1013,6 +1039,11 @@ kfp_status launch_fem_finish(kfp_problem pb, StepParams P, int nsub, int max_row
 
 // slab buffer that holds u(T) after a window: the last step's output (FD), or the fem_finish output
 int final_parity(const kfp_problem pb) { return (pb->nt + (pb->scheme == KFP_SCHEME_SPLIT_FEM ? 1 : 0)) & 1; }
+// u(T) slab of local descriptor ii after the last iteration
+const double *final_slab(const kfp_problem pb, size_t ii) {
+    if (pb->pipe > 1 && ii < pb->final_slab.size() && pb->final_slab[ii]) return pb->final_slab[ii];
+    return pb->subs[ii].slab[final_parity(pb)];
+}
 
 // Monodomain solve recording U at `lines` (BJ north_star (c)).
 kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
@@ -1213,6 +1244,13 @@ kfp_status kfp_problem_create_ex(const kfp_problem_desc *d, kfp_scheme scheme, k
     if (!st) st = up(&pb->d_u0v, d->u0v, (size_t)d->u0_rank * nn);
     if (!st) st = up(&pb->d_u0x, d->u0x, (size_t)d->u0_rank * d->nx);
     if (!st) st = up(reinterpret_cast<double **>(&pb->d_rowc), reinterpret_cast<const double *>(rowc.data()), 2 * nn);
+    {
+        std::vector<double> cfn((size_t)d->nt * kfp::kMaxRank, 0.0);
+        for (int n = 0; n < d->nt; ++n)
+            for (int r = 0; r < d->f_rank; ++r)  // the same product launch_step forms for P.cf
+                cfn[(size_t)n * kfp::kMaxRank + r] = pb->dt * pb->ft[(size_t)r * (d->nt + 1) + n + 1];
+        if (!st) st = up(&pb->d_cfn, cfn.data(), cfn.size());
+    }
     if (st) {
         kfp_problem_destroy(pb);
         return st;
@@ -1553,7 +1591,7 @@ kfp_status kfp_swr_batch_subdomain_uT(kfp_problem pb, int32_t rep, int32_t s, do
         return KFP_E_INVAL;
     }
     const SubDev &sd = pb->subs[(size_t)rep * pb->S + s];
-    KFP_CUDA(cudaMemcpyAsync(out, sd.slab[final_parity(pb)], sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
+    KFP_CUDA(cudaMemcpyAsync(out, final_slab(pb, (size_t)rep * pb->S + s), sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
                              cudaMemcpyDeviceToHost, pb->stream));
     KFP_CUDA(cudaStreamSynchronize(pb->stream));
     return KFP_OK;
@@ -1602,7 +1640,7 @@ kfp_status kfp_swr_set_schedule(kfp_problem pb, kfp_schedule schedule) {
         set_err("kfp_swr_set_schedule: unknown schedule %d", (int)schedule);
         return KFP_E_INVAL;
     }
-    if (schedule == KFP_GAUSS_SEIDEL && (pb->s_begin != 0 || pb->s_end != pb->S || pb->plan.window)) {
+    if (schedule == KFP_GAUSS_SEIDEL && (pb->s_begin != 0 || pb->s_end != pb->S || pb->plan.window || pb->pipe > 1)) {
         set_err("kfp_swr_set_schedule: Gauss-Seidel needs every subdomain on this process and a per-step plan");
         return KFP_E_INVAL;
     }
@@ -1639,6 +1677,59 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
     P.carry = pb->d_carry;
     P.ovrec = pb->ovrec ? 1 : 0;
     KFP_CUDA(cudaEventRecord(pb->ev[0], pb->stream));
+    if (pb->pipe > 1) {
+        // pipelined Jacobi: groups of up to D iterations in one sweep of nt + G - 1
+        // launches; slot d runs iteration k0 + d at step L - d, reading trace row L - d of iteration
+        // k0 + d - 1 (written by slot d - 1 one launch earlier) from the ring
+        const int D = pb->pipe, R = D + 1, ntot = nloc, nl = pb->s_end - pb->s_begin;
+        int it = 0, g = 0;
+        while (it < n_iter) {
+            const int G = std::min(D, n_iter - it), k0 = pb->k_done + 1;
+            for (int d = 0; d < G; ++d) {
+                const int k = k0 + d;
+                for (int ii = 0; ii < ntot; ++ii) {
+                    SubDev &sd = pb->psubs[(size_t)d * ntot + ii];
+                    const int r = ii / nl, i = ii % nl;
+                    if (i > 0) {
+                        sd.gL[0] = pb->ringR[(size_t)r * (nl - 1) + i - 1][(k - 1) % R];
+                        sd.sendL[0] = pb->ringL[(size_t)r * (nl - 1) + i - 1][k % R];
+                    }
+                    if (i < nl - 1) {
+                        sd.gR[0] = pb->ringL[(size_t)r * (nl - 1) + i][(k - 1) % R];
+                        sd.sendR[0] = pb->ringR[(size_t)r * (nl - 1) + i][k % R];
+                    }
+                    sd.grp = r * pb->K_max + (k - 1);  // error slot (err_stride 1)
+                }
+            }
+            KFP_CUDA(cudaMemcpyAsync(pb->d_psubs, pb->psubs.data(), sizeof(SubDev) * (size_t)G * ntot,
+                                     cudaMemcpyHostToDevice, pb->stream));
+            StepParams Pp = P;
+            Pp.subs = pb->d_psubs;
+            Pp.par_in = Pp.par_out = Pp.par_in_lo = 0;
+            Pp.errT = pb->d_errT;
+            Pp.errIF = pb->d_errIF;
+            Pp.err_stride = 1;
+            Pp.last = 1;  // errors at T on each slot's own last step
+            KFP_CUDA(cudaEventRecord(pb->ev[2 + 2 * g], pb->stream));
+            for (int L = 0; L < pb->nt + G - 1; ++L)
+                if (kfp_status st = launch_step(pb, pb->plan, Pp, G * ntot, L, pb->pfd, 0, nullptr, true)) return st;
+            if (pb->scheme == KFP_SCHEME_SPLIT_FEM) {
+                int rows = 0;
+                for (const SubDev &sd : pb->subs) rows = std::max(rows, sd.hi - sd.lo + 1);
+                if (kfp_status st = launch_fem_finish(pb, Pp, G * ntot, rows)) return st;
+            }
+            KFP_CUDA(cudaEventRecord(pb->ev[3 + 2 * g], pb->stream));
+            pb->final_slab.assign(ntot, nullptr);
+            for (int ii = 0; ii < ntot; ++ii) pb->final_slab[ii] = pb->psubs[(size_t)(G - 1) * ntot + ii].slab[final_parity(pb)];
+            KFP_CUDA(cudaStreamSynchronize(pb->stream));  // psubs is rewritten for the next group
+            pb->k_done += G;
+            it += G;
+            ++g;
+        }
+        pb->ev_used = 2 + 2 * g;
+        KFP_CUDA(cudaEventRecord(pb->ev[1], pb->stream));
+        return KFP_OK;
+    }
     for (int it = 0; it < n_iter; ++it) {
         const int k = pb->k_done + 1;  // 1-based iteration number
         P.par_in = (k - 1) & 1;
@@ -1660,7 +1751,7 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
                 if (fs.l2c) fs.l2c += (size_t)s * pl.C * kfp::kL2M;
                 if (fs.ctab) fs.ctab += (size_t)s * 4 * pl.P * kfp::kCT;
                 for (int n = 0; n < pb->nt; ++n) {
-                    Ps.last = (n + 1 == pb->nt);
+                    Ps.last = (n + 1 == pb->nt);  // (the cluster kernel tests its own step; see StepParams)
                     if (kfp_status st = launch_step(pb, pl, Ps, 1, n, fs)) return st;
                 }
             }
@@ -1690,13 +1781,95 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
     return KFP_OK;
 }
 
+kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth) {
+    if (!pb || !pb->setup) {
+        set_err("kfp_swr_set_pipeline: no setup");
+        return KFP_E_STATE;
+    }
+    if (depth < 1 || depth > 64) {
+        set_err("kfp_swr_set_pipeline: depth %d outside [1, 64]", depth);
+        return KFP_E_INVAL;
+    }
+    if (pb->k_done != 0) {
+        set_err("kfp_swr_set_pipeline: call right after setup / reset");
+        return KFP_E_STATE;
+    }
+    if (depth == pb->pipe) return KFP_OK;
+    const Plan &pl = pb->plan;
+    if (depth > 1 && (pb->gauss_seidel || pb->ovrec || pb->s_begin != 0 || pb->s_end != pb->S || !pl.fused || pl.col ||
+                      pl.window || pb->pipe != 1)) {
+        set_err("kfp_swr_set_pipeline: needs the Jacobi schedule, every subdomain on this process, the per-step "
+                "cluster kernel, no overlap recording, and a fresh setup (plan: %s)", pl.text.c_str());
+        return KFP_E_INVAL;
+    }
+    if (depth == 1) {
+        set_err("kfp_swr_set_pipeline: a pipelined setup cannot go back to depth 1; set it up again");
+        return KFP_E_INVAL;
+    }
+    {
+        FusedKernel k;
+        size_t smem = 0;
+        if (!fused_kernel(pl.B, pl.NR, pl.P, &k, &smem, pl.fem, true)) {
+            set_err("kfp_swr_set_pipeline: no pipelined kernel variant for this plan (%s)", pl.text.c_str());
+            return KFP_E_INVAL;
+        }
+        KFP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
+    KFP_CUDA(cudaSetDevice(pb->device));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));
+    const int D = depth, R = D + 1, ntot = (int)pb->subs.size(), nl = pb->s_end - pb->s_begin;
+    const size_t nx = pb->nx, TR = (size_t)pb->nt * nx;
+    // trace rings: slots 0 and 1 are the setup's parity buffers (slot 0 is what reset / set_initial_trace write)
+    pb->ringL.assign((size_t)pb->n_rep * (nl - 1), std::vector<double *>(R, nullptr));
+    pb->ringR.assign((size_t)pb->n_rep * (nl - 1), std::vector<double *>(R, nullptr));
+    for (int r = 0; r < pb->n_rep; ++r)
+        for (int i = 0; i + 1 < nl; ++i) {
+            const SubDev &left = pb->subs[(size_t)r * nl + i];
+            auto &rl = pb->ringL[(size_t)r * (nl - 1) + i], &rr = pb->ringR[(size_t)r * (nl - 1) + i];
+            for (int q = 0; q < 2; ++q) {
+                rl[q] = const_cast<double *>(left.gR[q]);
+                rr[q] = left.sendR[q];
+            }
+            for (int q = 2; q < R; ++q) {
+                if (kfp_status st = swr_alloc(pb, &rl[q], TR)) return st;
+                if (kfp_status st = swr_alloc(pb, &rr[q], TR)) return st;
+            }
+        }
+    // slot descriptors: slot 0 = the setup's subdomains; slots d > 0 get their own slabs
+    pb->psubs.assign((size_t)D * ntot, SubDev());
+    for (int d = 0; d < D; ++d)
+        for (int ii = 0; ii < ntot; ++ii) {
+            SubDev sd = pb->subs[ii];
+            sd.lag = d;
+            if (d > 0)
+                for (int q = 0; q < 2; ++q)
+                    if (kfp_status st = swr_alloc(pb, &sd.slab[q], (size_t)(sd.hi - sd.lo + 1) * nx)) return st;
+            pb->psubs[(size_t)d * ntot + ii] = sd;
+        }
+    {
+        void *q = nullptr;
+        KFP_CUDA(cudaMalloc(&q, sizeof(SubDev) * pb->psubs.size()));
+        pb->d_psubs = static_cast<SubDev *>(q);
+        pb->swr_allocs.push_back(static_cast<double *>(q));
+        std::vector<void *> own;
+        kfp_status st = build_tmaps(pb, pl, pb->psubs, &pb->pfd.maps, &own);
+        if (!st) st = build_l2m(pb, pl, pb->psubs, &pb->pfd.l2c, &own);
+        for (void *o : own) pb->swr_allocs.push_back(static_cast<double *>(o));
+        if (st) return st;
+        pb->pfd.coefT = pb->fd.coefT;
+        pb->pfd.tabs = pb->fd.tabs;
+    }
+    pb->pipe = D;
+    return KFP_OK;
+}
+
 kfp_status kfp_swr_set_overlap_error(kfp_problem pb, int32_t on) {
     if (!pb || !pb->setup) {
         set_err("kfp_swr_set_overlap_error: no setup");
         return KFP_E_STATE;
     }
     const Plan &pl = pb->plan;
-    if (on && (!pl.fused || pl.col || pl.window)) {
+    if (on && (!pl.fused || pl.col || pl.window || pb->pipe > 1)) {
         set_err("kfp_swr_set_overlap_error: needs the per-step cluster kernel (plan: %s)", pl.text.c_str());
         return KFP_E_INVAL;
     }
@@ -1848,12 +2021,11 @@ kfp_status kfp_swr_solve_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
     if (kfp_status st = kfp_swr_iterate(pb, K)) return st;
     if (uT) {
         const size_t nx = pb->nx;
-        const int par = final_parity(pb);
         for (int s = 0; s < n_sub; ++s) {
             const SubDev &sd = pb->subs[s];
             const int c0 = s * (pb->nv / n_sub);
             const int c1 = (s == n_sub - 1) ? pb->nv : (s + 1) * (pb->nv / n_sub) - 1;
-            KFP_CUDA(cudaMemcpyAsync(uT + (size_t)c0 * nx, sd.slab[par] + (size_t)(c0 - sd.lo) * nx,
+            KFP_CUDA(cudaMemcpyAsync(uT + (size_t)c0 * nx, final_slab(pb, s) + (size_t)(c0 - sd.lo) * nx,
                                      sizeof(double) * (size_t)(c1 - c0 + 1) * nx, cudaMemcpyDeviceToHost, pb->stream));
         }
     }
@@ -1898,7 +2070,7 @@ kfp_status kfp_swr_subdomain_uT(kfp_problem pb, int32_t s, double *out) {
         return KFP_E_INVAL;
     }
     const SubDev &sd = pb->subs[s - pb->s_begin];
-    KFP_CUDA(cudaMemcpyAsync(out, sd.slab[final_parity(pb)], sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
+    KFP_CUDA(cudaMemcpyAsync(out, final_slab(pb, s - pb->s_begin), sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
                              cudaMemcpyDeviceToHost, pb->stream));
     KFP_CUDA(cudaStreamSynchronize(pb->stream));
     return KFP_OK;
@@ -1912,6 +2084,10 @@ kfp_status kfp_swr_trace(kfp_problem pb, int32_t i, int32_t dir, double *out) {
     const int par = pb->k_done & 1;
     const SubDev &sd = pb->subs[i - pb->s_begin];
     const double *src = (dir == 0) ? sd.gR[par] : sd.sendR[par];
+    if (pb->pipe > 1) {  // the ring slot of the last iteration
+        const int R = pb->pipe + 1;
+        src = (dir == 0 ? pb->ringL : pb->ringR)[i - pb->s_begin][pb->k_done % R];
+    }
     KFP_CUDA(cudaMemcpyAsync(out, src, sizeof(double) * (size_t)pb->nt * pb->nx, cudaMemcpyDeviceToHost, pb->stream));
     KFP_CUDA(cudaStreamSynchronize(pb->stream));
     return KFP_OK;

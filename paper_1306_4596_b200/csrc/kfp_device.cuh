@@ -64,7 +64,12 @@ struct SubDev {
     // [lo_s, hi_{s-1}] shared with s-1, side 1 = [lo_{s+1}, hi_s] shared with s+1; ovn = 0: not recorded
     int ovr0[2], ovn[2];         // first node, node count
     double *ovb[2];              // [ovn][nt][nx] this subdomain's values there (u; split FEM: w)
+    // pipelined Jacobi iterations: this descriptor runs step P.n - lag of its
+    // iteration; outside [0, nt) the CTA exits (pipeline fill / drain).  0 otherwise.
+    int lag, pad2_;
+    double pad3_;                // keep sizeof % 16 == 0 (the column kernel bulk-copies descriptor arrays)
 };
+static_assert(sizeof(SubDev) % 16 == 0, "SubDev arrays are copied with cp.async.bulk (16-B granules)");
 
 struct StepParams {
     const SubDev *subs;
@@ -75,7 +80,7 @@ struct StepParams {
     int par_in_lo;         // parity of the incoming LEFT trace: par_in (Jacobi) or par_out
                            // (Gauss-Seidel SWR1-SWR4: the left neighbour already ran this iteration)
     int from_u0;           // n == 0: u^0 from the u0 tables (no slab read)
-    int last;              // n+1 == nt
+    int last;              // n+1 == nt (the cluster kernel: "errors at T wanted" -- it tests step == nt-1 itself)
     int send_robin;        // outgoing trace kind: 0 Dirichlet value, 1 Robin combination
     int f_rank, u0_rank;
     int P, b, R, C;        // warps per CTA, rows per chunk, rows per block, blocks per column
@@ -84,7 +89,8 @@ struct StepParams {
     int ovrec;             // record the overlap rows into SubDev::ovb (cluster kernel only)
     double q, a, qa, hv, dt, p;   // split FEM: a = tau/h_v^2 - 1/6, dt = tau
     double dnu, nu0;       // split FEM transport weight of node j: |j dnu + nu0| = |v_j| tau / h_x (0 at n = 0)
-    double cf[kMaxRank];   // dt * ft[r][n+1]
+    double cf[kMaxRank];   // dt * ft[r][n+1]  (window / column kernels)
+    const double *cfn;     // [nt][kMaxRank] dt * ft[r][n+1] per step (cluster kernel: steps differ per slot)
     const double2 *rowc;   // per node: (1-|nu_j|, |nu_j|)
     const double *fv;      // [f_rank][nv+1]
     const double *fx;      // [f_rank][nx]

@@ -290,7 +290,9 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 
 // --------------------------------------------------------------------------- the kernel
-template <int B, int NR, int P_, bool FEM = false>
+// PIPE: pipelined iterations -- every descriptor carries its own step (P.n - S.lag); otherwise the step
+// and its flags come from the launch parameters (constant bank, no registers held).
+template <int B, int NR, int P_, bool FEM = false, bool PIPE = false>
 __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const FusedParams FP) {
     constexpr int NW = P_;            // warps (= chunks) per CTA
     constexpr int kCPW = kWarp / NW;  // columns per warp in the transposed phase
@@ -310,6 +312,11 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
         __syncthreads();
     }
     const SubDev &S = sm.sd;
+    // the step this descriptor computes (pipelined iterations: each slot lags by S.lag steps); recomputed
+    // where used (constant bank + shared memory) rather than held in registers across the tile loop
+#define step (PIPE ? P.n - S.lag : P.n)
+#define from_u0 (PIPE ? step == 0 : P.from_u0 != 0)
+#define last (PIPE ? (P.last && step == P.nt - 1) : P.last != 0)  // pipelined: P.last = errors at T wanted
     const int n = S.n, L = FP.L, R = NW * L;
     const int rb0 = blk * R;                                    // first unknown row of this block
     const int Rb = max(0, min(R, n - rb0));                     // rows of this block
@@ -317,10 +324,11 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
     const int Lw = max(0, min(L, Rb - s_w));                    // rows of this warp's chunk
     const int cr0 = rb0 + s_w;                                  // first column row of the chunk
     const int nblk = S.nblk;
-    const bool live = blk < nblk;                               // the block holds rows of the column
+    // the block holds rows of the column, and the slot's step exists (pipeline fill / drain: whole cluster)
+    const bool live = blk < nblk && (!PIPE || (step >= 0 && step < P.nt));
     const double q = P.q;
-    const CUtensorMap *tmap = FP.tmaps + 2 * sub + (P.n & 1);
-    double *unew_slab = S.slab[(P.n + 1) & 1];
+    const CUtensorMap *tmap = FP.tmaps + 2 * sub + (step & 1);
+    double *unew_slab = S.slab[(step + 1) & 1];
     double *unew = unew_slab + static_cast<size_t>(S.first - S.lo) * P.nx;
     double *tile_w = sm.tile + warp * Sm::kSlot;
     double *coef_w = sm.coef + warp * B * Sm::kCoef;
@@ -365,10 +373,10 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
     }
     if (lane == 0 && Lw > 0) { // this chunk's per-row coefficients (+ its first u^n tile below)
         if (FEM) {
-            mbar_expect_tx(&sm.bar[warp], P.from_u0 ? 0u : tile_bytes);  // 0: completes phase 0 at once
+            mbar_expect_tx(&sm.bar[warp], from_u0 ? 0u : tile_bytes);  // 0: completes phase 0 at once
         } else {
             const uint32_t coef_bytes = static_cast<uint32_t>(Lw * Sm::kCoef * sizeof(double));
-            mbar_expect_tx(&sm.bar[warp], coef_bytes + (P.from_u0 ? 0u : tile_bytes));
+            mbar_expect_tx(&sm.bar[warp], coef_bytes + (from_u0 ? 0u : tile_bytes));
             bulk_g2s(coef_w, FP.coefT + static_cast<size_t>(S.first + cr0) * Sm::kCoef, coef_bytes, &sm.bar[warp]);
         }
     }
@@ -378,7 +386,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
         bulk_g2s(sm.l2m, FP.l2m + (static_cast<size_t>(sub) * P.C + blk) * kL2M, kL2M * sizeof(double), &sm.tbar);
     }
     grid_dep_wait();  // the previous step's u^n is complete
-    if (Lw > 0 && !P.from_u0 && lane == 0 && t_first < FP.ntiles)
+    if (Lw > 0 && !from_u0 && lane == 0 && t_first < FP.ntiles)
         tma_load_2d(tile_w, tmap, t_first * kWarp - kHalo, ty0, &sm.bar[warp]);
     cluster_wait();  // matches the prologue arrive
     KFP_T(1)
@@ -390,10 +398,11 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
         const int m0 = t * kWarp, w = min(kWarp, P.nx - m0);
         const int m = m0 + min(lane, w - 1);
         const bool active = lane < w;
-        const size_t goff = static_cast<size_t>(P.n) * P.nx + m;   // row t_{n+1} of [nt][nx] arrays
+        const size_t goff = static_cast<size_t>(step) * P.nx + m;  // row t_{n+1} of [nt][nx] arrays
         double fx[NR];  // this lane's forcing profile times dt ft_r(t_{n+1})
 #pragma unroll
-        for (int r = 0; r < NR; ++r) fx[r] = (r < P.f_rank) ? P.cf[r] * __ldg(P.fx + r * P.nx + m) : 0.0;
+        for (int r = 0; r < NR; ++r)
+            fx[r] = (r < P.f_rank) ? (PIPE ? __ldg(P.cfn + step * kMaxRank + r) : P.cf[r]) * __ldg(P.fx + r * P.nx + m) : 0.0;
         if (warp == 0) {  // incoming traces of this step (written by the previous iteration)
             sm.gin[lane] = (S.ltype == END_DIRI || S.ltype == END_ROBIN) ? S.gL[P.par_in_lo][goff] : 0.0;
             sm.gin[kWarp + lane] = (S.rtype == END_DIRI || S.rtype == END_ROBIN) ? S.gR[P.par_in][goff] : 0.0;
@@ -403,9 +412,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
         double h[B];
         double hend = 0.0, kst = 0.0;
         if (Lw > 0) {
-            if (!P.from_u0 || it == 0) mbar_wait(&sm.bar[warp], par);
+            if (!from_u0 || it == 0) mbar_wait(&sm.bar[warp], par);
             KFP_TT(0)
-            if (P.from_u0) {  // u^0 from the separable u0 tables (0 B of HBM), incl. the halo columns
+            if (from_u0) {  // u^0 from the separable u0 tables (0 B of HBM), incl. the halo columns
                 for (int l = 0; l < Lw + 2 * kX; ++l) {
                     const int j = KFP_JB + l;
                     if (FEM && (j < S.lo || j > S.hi)) continue;  // ghost row outside the subdomain (set below)
@@ -421,7 +430,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             } else if (m0 == 0 || m0 + w == P.nx) {
                 // periodic wrap of the halo at the ends of the x range (TMA zero-fills out-of-range columns)
                 const int jb = KFP_JB;
-                const double *src = S.slab[P.n & 1] + static_cast<ptrdiff_t>(jb - S.lo) * P.nx;
+                const double *src = S.slab[step & 1] + static_cast<ptrdiff_t>(jb - S.lo) * P.nx;
                 // one row per lane, strided: a chunk may hold more rows (L <= 33) than a warp has lanes
                 for (int l = lane; l < Lw + 2 * kX; l += kWarp) {
                     if (FEM && (jb + l < S.lo || jb + l > S.hi)) continue;
@@ -437,13 +446,14 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             // last two rows takes the ragged one (it captures their k values)
             const bool full = (Lw == B) && (cr0 + Lw <= n - 2);
             if (FEM) {
-                const double c1 = P.qa * (1.0 / 6.0), c4 = 4.0 * c1, vb = fma(static_cast<double>(jb), P.dnu, P.nu0);
+                const double dnu = from_u0 ? 0.0 : P.dnu, nu0 = from_u0 ? 0.0 : P.nu0;  // step 0: u0, no Step 2
+                const double c1 = P.qa * (1.0 / 6.0), c4 = 4.0 * c1, vb = fma(static_cast<double>(jb), dnu, nu0);
                 // unknown end nodes (Neumann / Robin ends) in this chunk: reflected ghosts
                 const bool gtop = cr0 == 0 && S.first == S.lo;
                 const int gl = (cr0 + Lw == n && S.first + n - 1 == S.hi) ? Lw - 1 : -1;
-                if (full && jv2_0 >= 0) pass_a_fem<B, -1>(tile_w, lane, q, c1, c4, vb, P.dnu, jv2_0, h, Lw, hend, gtop, gl);
-                else if (full && jv2_1 < 0) pass_a_fem<B, 1>(tile_w, lane, q, c1, c4, vb, P.dnu, jv2_0, h, Lw, hend, gtop, gl);
-                else pass_a_fem<B, 0>(tile_w, lane, q, c1, c4, vb, P.dnu, jv2_0, h, Lw, hend, gtop, gl);
+                if (full && jv2_0 >= 0) pass_a_fem<B, -1>(tile_w, lane, q, c1, c4, vb, dnu, jv2_0, h, Lw, hend, gtop, gl);
+                else if (full && jv2_1 < 0) pass_a_fem<B, 1>(tile_w, lane, q, c1, c4, vb, dnu, jv2_0, h, Lw, hend, gtop, gl);
+                else pass_a_fem<B, 0>(tile_w, lane, q, c1, c4, vb, dnu, jv2_0, h, Lw, hend, gtop, gl);
             } else {
                 if (full && jv2_0 >= 0) pass_a_reg<B, NR, -1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
                 else if (full && jv2_1 < 0) pass_a_reg<B, NR, 1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
@@ -457,10 +467,10 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                         // one-sided mass average (2 u_c + u_nb) / 3 of the transported rows at the trace node
                         // c and its neighbour toward the sender's interior (reading F4)
                         const int i = itr - cr0 + 1, inb = side ? i - 1 : i + 1, jb = KFP_JB;
-                        const double vb = fma(static_cast<double>(jb), P.dnu, P.nu0);
+                        const double dnu = from_u0 ? 0.0 : P.dnu, vb = from_u0 ? 0.0 : fma(static_cast<double>(jb), P.dnu, P.nu0);
                         auto trr = [&](int ii) {
                             const double *row = tile_w + ii * kTW + kHalo + lane;
-                            const double nu = fabs(fma(static_cast<double>(ii), P.dnu, vb));
+                            const double nu = fabs(fma(static_cast<double>(ii), dnu, vb));
                             return fma(nu, row[(2 * (jb + ii) - P.nv >= 0) ? -1 : 1] - row[0], row[0]);
                         };
                         sm.rtr[par][side * kWarp + lane] = (2.0 * trr(i) + trr(inb)) * (1.0 / 3.0);
@@ -477,7 +487,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             }
             // the slot is consumed: prefetch this warp's chunk of the next tile
             __syncwarp();
-            if (lane == 0 && !P.from_u0 && t + FP.Gc < FP.ntiles) {
+            if (lane == 0 && !from_u0 && t + FP.Gc < FP.ntiles) {
                 fence_proxy_async_smem();
                 mbar_expect_tx(&sm.bar[warp], tile_bytes);
                 tma_load_2d(tile_w, tmap, (t + FP.Gc) * kWarp - kHalo, ty0, &sm.bar[warp]);
@@ -619,7 +629,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                         if (l < Lw) dst[l * pitch] = h[l];
                 }
             }
-            if (!FEM && P.last && active) {  // error at T on every unknown row (a 1/N_t fraction of the steps)
+            if (!FEM && last && active) {  // error at T on every unknown row (a 1/N_t fraction of the steps)
                 const double *ut = P.UT + static_cast<size_t>(S.first + cr0) * P.nx + m;
 #pragma unroll
                 for (int l = 0; l < B; ++l)
@@ -639,27 +649,27 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             if (blk == 0 && S.ltype == END_DIRI) {
                 const double g = sm.gin[lane];
                 if (S.iL_tr == -1) S.sendL[P.par_out][goff] = g;  // no overlap: the end node is the trace node
-                if (S.ifL >= 0) eif = fmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + m]));
+                if (S.ifL >= 0) eif = fmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + step) * P.nx + m]));
                 if (FEM) {  // the node's value enters the next step's transport and mass average
                     unew_slab[m] = g;
-                } else if (P.last) {
+                } else if (last) {
                     et = fmax(et, fabs(g - P.UT[static_cast<size_t>(S.lo) * P.nx + m]));
                     unew_slab[m] = g;
                 }
-            } else if (blk == 0 && S.ltype == END_PHYS && P.last) {
+            } else if (blk == 0 && S.ltype == END_PHYS && last) {
                 unew_slab[m] = 0.0;
             }
             if (blk == nblk - 1 && S.rtype == END_DIRI) {
                 const double g = sm.gin[kWarp + lane];
                 if (S.iR_tr == n) S.sendR[P.par_out][goff] = g;
-                if (S.ifR >= 0) eif = fmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + m]));
+                if (S.ifR >= 0) eif = fmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + step) * P.nx + m]));
                 if (FEM) {
                     unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + m] = g;
-                } else if (P.last) {
+                } else if (last) {
                     et = fmax(et, fabs(g - P.UT[static_cast<size_t>(S.hi) * P.nx + m]));
                     unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + m] = g;
                 }
-            } else if (blk == nblk - 1 && S.rtype == END_PHYS && P.last) {
+            } else if (blk == nblk - 1 && S.rtype == END_PHYS && last) {
                 unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + m] = 0.0;
             }
         }
@@ -688,14 +698,14 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                     S.sendR[P.par_out][goff] = g;
                 }
                 if (inblk(sp_row[4]))
-                    eif = fmax(eif, fabs(sm.xsp[4 * kWarp + lane] - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + m]));
+                    eif = fmax(eif, fabs(sm.xsp[4 * kWarp + lane] - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + step) * P.nx + m]));
                 if (inblk(sp_row[5]))
-                    eif = fmax(eif, fabs(sm.xsp[5 * kWarp + lane] - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + m]));
+                    eif = fmax(eif, fabs(sm.xsp[5 * kWarp + lane] - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + step) * P.nx + m]));
                 if (P.record)  // read back this block's recorded rows of u^{n+1} (stored above by this CTA)
                     for (int i = 0; i < FP.nrec; ++i) {
                         const int row = FP.rec_rows[i];
                         if (inblk(row))
-                            P.rec[(static_cast<size_t>(i) * P.nt + P.n) * P.nx + m] = unew[static_cast<size_t>(row) * P.nx + m];
+                            P.rec[(static_cast<size_t>(i) * P.nt + step) * P.nx + m] = unew[static_cast<size_t>(row) * P.nx + m];
                     }
                 if (P.ovrec)  // this subdomain's overlap rows (unknown rows of this block; Dirichlet end nodes)
                     for (int side = 0; side < 2; ++side)
@@ -707,7 +717,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                             else if (node == S.lo && S.ltype == END_DIRI && blk == 0) val = sm.gin[lane];
                             else if (node == S.hi && S.rtype == END_DIRI && blk == nblk - 1) val = sm.gin[kWarp + lane];
                             else have = false;
-                            if (have) S.ovb[side][(static_cast<size_t>(r) * P.nt + P.n) * P.nx + m] = val;
+                            if (have) S.ovb[side][(static_cast<size_t>(r) * P.nt + step) * P.nx + m] = val;
                         }
             }
         }
@@ -738,6 +748,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
     KFP_T(63)
 }
 #undef KFP_JB
+#undef step
+#undef from_u0
+#undef last
 
 // Split FEM: the slab after the window's last step holds w^{nt-1/2}; the scheme's
 // u(T) is its last Step 2, u_j(x_m) = w_j + nu_j (w_j(x_nb) - w_j(x_m)).  One pass over

@@ -43,7 +43,11 @@ class CudaBlock:
         self.n_sub = n_sub
         g = prob.grid
         torch.cuda.set_device(device)
-        self.stream = torch.cuda.current_stream()
+        # a real stream made current: the library's launches, torch's NCCL exchange (which orders itself
+        # after the current stream) and the timing events all sit on it (the legacy default stream, handle 0,
+        # would leave the library on its own non-blocking stream, unordered with the exchange)
+        self.stream = torch.cuda.Stream(device=device)
+        torch.cuda.set_stream(self.stream)
         self.pb = Problem(prob, device=device)
         self.pb.set_stream(self.stream.cuda_stream)
         self.pb.setup(kind, p, overlap, n_sub, K, self.s_begin, self.s_end, q=q)
@@ -124,14 +128,16 @@ def bench_main(args, default_workload, clock_sampler=None, peaks=None):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    os.environ.setdefault("NCCL_DEBUG", "WARN")  # rank 0's stdout carries exactly one JSON line
+    # rank 0's stdout carries exactly one JSON line (bench.py points file descriptor 1 at stderr for native
+    # output such as NCCL's banner and prints the line through a duplicate of the original stdout)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
     run = ki.config(args.workload or default_workload(world))
     g = run.grid
     prob = ki.make_problem(run)
     blk = CudaBlock(prob, run.kind, run.p, run.overlap, run.n_sub, run.K, rank, world, local)
-    stream = torch.cuda.current_stream()
+    stream = blk.stream  # current (CudaBlock made it so)
 
     kernel_ms = [0.0]
 

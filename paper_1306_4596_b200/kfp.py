@@ -27,7 +27,7 @@ SYMBOLS = (
     "kfp_swr_reset", "kfp_swr_iterate", "kfp_swr_edge_buffers", "kfp_swr_bind_edge_buffers", "kfp_swr_solve", "kfp_error_history",
     "kfp_swr_subdomain_uT", "kfp_swr_subdomain_range", "kfp_swr_trace", "kfp_monodomain_uT", "kfp_launch_count",
     "kfp_plan", "kfp_last_timing", "kfp_last_error",
-    "kfp_swr_set_overlap_error", "kfp_swr_overlap_history", "kfp_swr_iterate_until",
+    "kfp_swr_set_overlap_error", "kfp_swr_overlap_history", "kfp_swr_iterate_until", "kfp_swr_set_pipeline",
 )
 
 
@@ -93,6 +93,7 @@ def load(path: str = LIB_PATH):
         "kfp_last_timing": (i32, [vp, pd, pd]),
         "kfp_last_error": (ctypes.c_char_p, []),
         "kfp_swr_set_overlap_error": (i32, [vp, i32]),
+        "kfp_swr_set_pipeline": (i32, [vp, i32]),
         "kfp_swr_overlap_history": (i32, [vp, i32, i32, ctypes.POINTER(i32), vp]),
         "kfp_swr_iterate_until": (i32, [vp, i32, dbl, i32, ctypes.POINTER(i32)]),
     }
@@ -270,6 +271,10 @@ class Problem:
     def set_overlap_error(self, on: bool = True):
         """Record the paper's convergence quantity max |u_s - u_{s+1}| over the overlaps."""
         _check(load().kfp_swr_set_overlap_error(self._h, 1 if on else 0))
+
+    def set_pipeline(self, depth: int):
+        """Pipelined Jacobi: advance `depth` consecutive iterations per sweep of nt + depth - 1 launches."""
+        _check(load().kfp_swr_set_pipeline(self._h, int(depth)))
 
     def overlap_history(self, rep: int = 0):
         k = ctypes.c_int32(0)

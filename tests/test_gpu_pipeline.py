@@ -1,0 +1,106 @@
+"""-m gpu: pipelined Jacobi iterations (kfp_swr_set_pipeline) are bitwise the
+unpipelined ones -- the same per-tile arithmetic, only the launch schedule changes: slot d of a sweep runs
+iteration k0 + d at step L - d, reading trace row L - d of iteration k0 + d - 1 from a ring of buffers --
+and the first case is also checked against the oracle."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import kfp_inputs as ki
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def kfp():
+    from paper_1306_4596_b200 import build, kfp as k
+
+    build.build()
+    k.load()
+    return k
+
+
+RUNS = {
+    "c0": ki.config("c0"),
+    "c1_K12": ki.config("c1").with_(K=12),
+    "ragged_dirichlet_ov": ki.scaled(ki.config("c1"), nx=38, nv=96, nt=200, K=8, name="rd").with_(n_sub=4, overlap=6),
+    "oswr_pq_S3": ki.config("c0").with_(name="pq3", p=2.5, q=0.4, K=7, n_sub=4),
+    "c4_small": ki.scaled(ki.config("c4"), nx=64, nv=32 * 32, nt=60, K=6, name="c4_small"),
+    "fem_paper_j0": ki.Run("fem_j0", ki.paper_grid(0), "random_u0", "robin", 11.0, 3, 2, 7, q=2.5, scheme="split_fem"),
+    "fem_dirichlet": ki.Run("fem_d", ki.Grid(64, 200, 40, 1.0, 0.4), "random_u0", "dirichlet", 0.0, 2, 4, 6,
+                            scheme="split_fem"),
+}
+
+
+def _solve(kfp, run, depth, lam=None):
+    with kfp.Problem(ki.make_problem(run)) as pb:
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
+        if depth > 1:
+            pb.set_pipeline(depth)
+        pb.reset()
+        if lam is not None:
+            for i in range(run.n_sub - 1):
+                pb.set_initial_trace(i, 0, lam[0][i])
+                pb.set_initial_trace(i, 1, lam[1][i])
+        pb.iterate(run.K)
+        eT, eI = pb.history()
+        return dict(eT=eT, eI=eI, slabs=[pb.subdomain_uT(s) for s in range(run.n_sub)],
+                    traces=[pb.trace(i, d) for i in range(run.n_sub - 1) for d in (0, 1)], launches=pb.launch_count())
+
+
+@pytest.mark.parametrize("name", list(RUNS))
+@pytest.mark.parametrize("depth", [2, 3, 64])
+def test_pipelined_equals_unpipelined(kfp, name, depth):
+    run = RUNS[name]
+    a, b = _solve(kfp, run, 1), _solve(kfp, run, min(depth, run.K))
+    assert np.array_equal(a["eT"], b["eT"]) and np.array_equal(a["eI"], b["eI"]), (name, a["eI"], b["eI"])
+    for x, y in zip(a["slabs"], b["slabs"]):
+        assert np.array_equal(x, y), name
+    for x, y in zip(a["traces"], b["traces"]):
+        assert np.array_equal(x, y), name
+
+
+def test_pipelined_random_initial_traces_vs_oracle(kfp):
+    """Random lambda^0 through the pipelined path (the ring's slot 0) against the oracle."""
+    import oracle
+
+    run = ki.Run("fem_lam", ki.Grid(64, 198, 30, 1.0, 0.3), "zero", "robin", 4.23, 3, 3, 6, scheme="split_fem")
+    g = run.grid
+    rng = np.random.default_rng(9)
+    lam = (rng.uniform(-1, 1, size=(run.n_sub - 1, g.nt, g.nx)), rng.uniform(-1, 1, size=(run.n_sub - 1, g.nt, g.nx)))
+    b = _solve(kfp, run, 4, lam)
+    r = oracle.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, run.K, init_traces=lam)
+
+    def rel(x, y):
+        return float(np.abs(np.asarray(x) - y).max() / np.abs(y).max())
+
+    assert rel(b["eT"], r["err_T"]) <= 1e-9 and rel(b["eI"], r["err_if"]) <= 1e-9
+    for x, y in zip(b["slabs"], r["uT_sub"]):
+        assert rel(x, y) <= 1e-9
+
+
+def test_pipeline_launch_count(kfp):
+    """One sweep of nt + depth - 1 step launches per group of depth iterations (+ nothing else for IMEX FD)."""
+    run = RUNS["c0"]
+    a, b = _solve(kfp, run, 1), _solve(kfp, run, run.K)
+    g = run.grid
+    mono = g.nt  # the monodomain reference at setup
+    assert a["launches"] - mono == g.nt * run.K
+    assert b["launches"] - mono == g.nt + run.K - 1
+
+
+def test_pipeline_rejected_combinations(kfp):
+    run = RUNS["c0"]
+    with kfp.Problem(ki.make_problem(run)) as pb:
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        pb.set_schedule("gauss_seidel")
+        with pytest.raises(kfp.KfpError):
+            pb.set_pipeline(4)
+    with kfp.Problem(ki.make_problem(run)) as pb:
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        pb.set_pipeline(4)
+        with pytest.raises(kfp.KfpError):
+            pb.set_schedule("gauss_seidel")
+        with pytest.raises(kfp.KfpError):
+            pb.set_overlap_error(True)
