@@ -232,10 +232,12 @@ Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool al
     // P = 8 warps (2 CTAs per SM) first, then P = 16 (1 CTA per SM): the smallest cluster whose
     // warps hold at most 33 rows; the column's first/last row blocks must hold >= 2 rows.
     const char *force = getenv("KFP_FORCE_P");  // debugging / experiments only
+    const char *forceC = getenv("KFP_FORCE_C");  // debugging / experiments only
     for (int P : {8, 16}) {
         if (force && atoi(force) != P) continue;
         int C = 1;
         while (C < 8 && (n_max + P * C - 1) / (P * C) > 33) ++C;
+        if (forceC && atoi(forceC) >= C && atoi(forceC) <= 8) C = atoi(forceC);
         int L = (n_max + P * C - 1) / (P * C);
         for (bool ok = false; !ok && L <= 33;) {
             ok = true;
