@@ -24,6 +24,9 @@ RUNS = {
     "dirichlet4": ki.scaled(ki.config("c4"), nx=16, nv=64, nt=30, K=5).with_(n_sub=4, overlap=4),
     # two-sided OSWR(p, q): the traces that cross the rank boundary carry q one way and p the other
     "robin_pq4": ki.scaled(ki.config("c3"), nx=16, nv=64, nt=30, K=5).with_(n_sub=4, p=3.0, q=0.8),
+    # the paper's split-FEM scheme: the driver moves the same trace bytes
+    "fem_robin_pq4": ki.Run("fem_pq4", ki.Grid(16, 64, 30, 1.0, 0.3), "random_u0", "robin", 4.23, 2, 4, 5, q=2.5,
+                            scheme="split_fem"),
 }
 
 
