@@ -346,6 +346,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
 #pragma unroll
     for (int qq = 0; qq < 6; ++qq) chunk_special |= sp_row[qq] >= cr0 && sp_row[qq] < cr0 + Lw;
     bool cta_special = trace_cta || P.record || P.ovrec;
+#ifdef KFP_ABLATE_SPECIAL  // experiments only (results invalid): no special-rows block
+    cta_special = false;
+#endif
 #pragma unroll
     for (int qq = 4; qq < 6; ++qq) cta_special |= inblk(sp_row[qq]);
     const int t_first = blockIdx.y;
