@@ -148,8 +148,19 @@ def bench_main(args, default_workload, clock_sampler=None, peaks=None):
         b.reset()
         return run_swr(b, run.K, rank, world, tally if timed else None)
 
+    # W untimed warm-up solves, then more until >= 5 s of warm-up (as bench.py); every rank runs the same
+    # count (the ranks exchange traces), agreed by a MAX all-reduce
+    t_w = time.perf_counter()
     for _ in range(args.warmup):
         one(blk)
+    torch.cuda.synchronize()
+    per = (time.perf_counter() - t_w) / max(1, args.warmup)
+    extra = torch.tensor([min(200, max(0, int((5.0 - (time.perf_counter() - t_w)) / max(per, 1e-3)) + 1))],
+                         device=dev, dtype=torch.int64)
+    dist.all_reduce(extra, op=dist.ReduceOp.MAX)
+    for _ in range(int(extra.item())):
+        one(blk)
+    warm = args.warmup + int(extra.item())
     dist.barrier()
     torch.cuda.synchronize()
     clocks = clock_sampler(local) if clock_sampler else None
@@ -200,7 +211,7 @@ def bench_main(args, default_workload, clock_sampler=None, peaks=None):
         peak, peak_kind = peaks() if peaks else (None, None)
         line = {
             "metric": "grid-point updates/s (N_x*N_v*N_t*K / wall)", "value": value, "unit": "updates/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "n_gpus": world, "steps": args.steps, "warmup": warm, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": run.name, "nx": g.nx, "nv": g.nv, "nt": g.nt, "K": run.K, "n_sub": run.n_sub,
                        "kind": run.kind, "overlap": run.overlap, "plan": plan,
