@@ -220,3 +220,28 @@ def test_iterate_until_tolerance(kfp):
         eo = pb.overlap_history()
     assert k == k_ref, (k, k_ref, r["err_ov"])
     assert rel(eo, r["err_ov"][:k]) <= TOL
+
+
+def test_fem_paper_j4_full_size_properties(kfp):
+    """The paper's finest Table 1 mesh (j = 4: 1600 x 3200 cells, 3200 steps) on the GPU, checked by
+    properties that hold at any size: the monodomain conserves sum_j (M 1)_j sum_m u_jm exactly (Neumann ends,
+    periodic x; pinned on CPU in test_fem_mass_is_conserved) and obeys the maximum principle; the SWR iterates
+    (Jacobi, OSWR(11, 2.5), overlap 3) approach it, and the paper's overlap quantity decreases."""
+    g = ki.paper_grid(4)
+    prob = ki.fem_problem(g, 3)
+    u0 = prob.u0_dense()
+    with kfp.Problem(prob) as pb:
+        UT = pb.monodomain()
+        pb.setup("robin", 11.0, 3, 2, 6, q=2.5)
+        pb.set_overlap_error(True)
+        pb.reset()
+        pb.iterate(6)
+        eT, eI = pb.history()
+        eo = pb.overlap_history()
+    wts = np.full(g.nv + 1, 2.0 / g.nv)
+    wts[[0, -1]] *= 0.5
+    m0, m1 = wts @ u0.sum(axis=1), wts @ UT.sum(axis=1)
+    assert abs(m1 - m0) <= 1e-12 * (wts @ np.abs(u0).sum(axis=1)), (m0, m1)
+    assert np.abs(UT).max() <= np.abs(u0).max() * (1 + 1e-13)
+    assert np.all(np.diff(eo) < 0) and eo[-1] < 0.3 * eo[0], eo  # Jacobi: ~0.7x per iteration here
+    assert eI[-1] < 0.3 * eI[0], (eT, eI)
