@@ -248,17 +248,24 @@ kfp_status kfp_swr_overlap_history(kfp_problem pb, int32_t rep, int32_t cap, int
  * only trace row n of iteration k, so one sweep of nt + depth - 1 launches advances `depth` consecutive
  * iterations, slot d running iteration k0 + d at step L - d in launch L.  Results are identical to the
  * unpipelined schedule (bitwise: same per-tile arithmetic); latency-bound small problems gain up to
- * depth x parallelism per launch.  Allocates (depth - 1) extra slabs per subdomain and depth + 1 trace
- * buffers per interface and direction.  depth >= 2 needs a fresh setup (call right after setup /
- * reset), the Jacobi schedule, every subdomain on this process, the per-step cluster kernel and no
- * overlap recording -> else KFP_E_INVAL / KFP_E_STATE.  kfp_swr_iterate then runs in groups of <= depth
- * iterations (one host synchronisation per group); kfp_last_timing reports per-group windows. */
+ * depth x parallelism per launch.  With the Gauss-Seidel schedule (SWR1-SWR4) the same sweep is a
+ * wavefront: subdomain s of slot d runs step L - (2 d + s) (its left trace, same iteration, was written
+ * one launch earlier by s - 1; its right trace by s + 1 of the previous iteration), so the serial
+ * schedule runs its subdomains concurrently; results are again bitwise the unpipelined schedule's.
+ * Allocates (depth - 1) extra slabs per subdomain and depth + 1 trace buffers per interface and
+ * direction.  depth >= 2 needs a fresh setup (call right after setup / reset), every subdomain on this
+ * process, the per-step cluster kernel and no overlap recording -> else KFP_E_INVAL / KFP_E_STATE.
+ * kfp_swr_iterate then runs in groups of <= depth iterations (one host synchronisation per group);
+ * kfp_last_timing reports per-group windows. */
 kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth);
 
-/* Tolerance stopping: run single iterations until `metric` of the last one (replica 0) is
- * below eps (or not finite), or k_max more iterations have run; *k_out = iterations done since the last
- * reset.  Each iteration synchronises the stream once to read its error (8 bytes).  KFP_E_STATE if
- * k_done + k_max > K_max or KFP_ERR_OVERLAP without recording. */
+/* Tolerance stopping: run iterations until `metric` of one of them (replica 0) is below eps
+ * (or not finite), or k_max more iterations have run; *k_out = the first iteration (counted since the
+ * last reset) that met the tolerance, else the iterations done.  Unpipelined: one iteration at a time,
+ * one stream synchronisation each (8 bytes read).  Pipelined (kfp_swr_set_pipeline): whole groups of
+ * up to depth iterations, so up to depth - 1 iterations beyond *k_out may have run (kfp_error_history
+ * and the solution reflect all that ran).  KFP_E_STATE if k_done + k_max > K_max or KFP_ERR_OVERLAP
+ * without recording. */
 kfp_status kfp_swr_iterate_until(kfp_problem pb, kfp_metric metric, double eps, int32_t k_max, int32_t *k_out);
 
 /* Copy the local subdomain s's current u_s(T) slab [(hi_s-lo_s+1)*nx] to host

@@ -361,6 +361,7 @@ struct kfp_problem_s {
     FusedData pfd;                         // tensor maps / level-2 maps of psubs (tables shared with fd)
     std::vector<std::vector<double *>> ringL, ringR;  // [rep * (nloc-1) + i][D+1]: sent left / right
     std::vector<const double *> final_slab;           // [ntot] u(T) of the last iteration (pipelined)
+    int2 *d_ppairs = nullptr;                         // [D][npairs] overlap pairs of the slot descriptors
     Plan plan;
     double *d_blkagg = nullptr, *d_chkagg = nullptr, *d_carry = nullptr;
     FusedData fd;                    // fused-kernel tensor maps and tables of the SWR setup
@@ -408,6 +409,7 @@ void free_swr(kfp_problem pb) {
     pb->ringL.clear();
     pb->ringR.clear();
     pb->final_slab.clear();
+    pb->d_ppairs = nullptr;
     pb->d_blkagg = pb->d_chkagg = pb->d_carry = nullptr;
     pb->fd = FusedData();
     for (int q = 0; q < 2; ++q) pb->edge_sendL[q] = pb->edge_recvL[q] = pb->edge_sendR[q] = pb->edge_recvR[q] = nullptr;
@@ -1642,7 +1644,7 @@ kfp_status kfp_swr_set_schedule(kfp_problem pb, kfp_schedule schedule) {
         set_err("kfp_swr_set_schedule: unknown schedule %d", (int)schedule);
         return KFP_E_INVAL;
     }
-    if (schedule == KFP_GAUSS_SEIDEL && (pb->s_begin != 0 || pb->s_end != pb->S || pb->plan.window || pb->pipe > 1)) {
+    if (schedule == KFP_GAUSS_SEIDEL && (pb->s_begin != 0 || pb->s_end != pb->S || pb->plan.window)) {
         set_err("kfp_swr_set_schedule: Gauss-Seidel needs every subdomain on this process and a per-step plan");
         return KFP_E_INVAL;
     }
@@ -1680,10 +1682,13 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
     P.ovrec = pb->ovrec ? 1 : 0;
     KFP_CUDA(cudaEventRecord(pb->ev[0], pb->stream));
     if (pb->pipe > 1) {
-        // pipelined Jacobi: groups of up to D iterations in one sweep of nt + G - 1
-        // launches; slot d runs iteration k0 + d at step L - d, reading trace row L - d of iteration
-        // k0 + d - 1 (written by slot d - 1 one launch earlier) from the ring
+        // pipelined iterations: groups of up to D iterations in one sweep of launches.
+        // Jacobi: slot d runs iteration k0 + d at step L - d, reading trace row L - d of iteration
+        // k0 + d - 1 (written by slot d - 1 one launch earlier) from the ring.  Gauss-Seidel (SWR1-SWR4):
+        // subdomain s of slot d lags 2 d + s steps -- its left trace (same iteration) was written by s - 1 one
+        // launch earlier, its right trace (previous iteration) by s + 1 of slot d - 1 one launch earlier.
         const int D = pb->pipe, R = D + 1, ntot = nloc, nl = pb->s_end - pb->s_begin;
+        const bool gs = pb->gauss_seidel;
         int it = 0, g = 0;
         while (it < n_iter) {
             const int G = std::min(D, n_iter - it), k0 = pb->k_done + 1;
@@ -1692,8 +1697,9 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
                 for (int ii = 0; ii < ntot; ++ii) {
                     SubDev &sd = pb->psubs[(size_t)d * ntot + ii];
                     const int r = ii / nl, i = ii % nl;
+                    sd.lag = gs ? 2 * d + i : d;
                     if (i > 0) {
-                        sd.gL[0] = pb->ringR[(size_t)r * (nl - 1) + i - 1][(k - 1) % R];
+                        sd.gL[0] = pb->ringR[(size_t)r * (nl - 1) + i - 1][(gs ? k : k - 1) % R];
                         sd.sendL[0] = pb->ringL[(size_t)r * (nl - 1) + i - 1][k % R];
                     }
                     if (i < nl - 1) {
@@ -1713,12 +1719,19 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
             Pp.err_stride = 1;
             Pp.last = 1;  // errors at T on each slot's own last step
             KFP_CUDA(cudaEventRecord(pb->ev[2 + 2 * g], pb->stream));
-            for (int L = 0; L < pb->nt + G - 1; ++L)
+            const int max_lag = gs ? 2 * (G - 1) + (nl - 1) : G - 1;
+            for (int L = 0; L < pb->nt + max_lag; ++L)
                 if (kfp_status st = launch_step(pb, pb->plan, Pp, G * ntot, L, pb->pfd, 0, nullptr, true)) return st;
             if (pb->scheme == KFP_SCHEME_SPLIT_FEM) {
                 int rows = 0;
                 for (const SubDev &sd : pb->subs) rows = std::max(rows, sd.hi - sd.lo + 1);
                 if (kfp_status st = launch_fem_finish(pb, Pp, G * ntot, rows)) return st;
+            }
+            if (pb->ovrec && pb->npairs > 0) {  // err_ov of every iteration of the group (slot grp = its slot)
+                kfp::overlap_diff<<<dim3(64, 1, G * pb->npairs), 256, 0, pb->stream>>>(pb->d_psubs, pb->d_ppairs, pb->nt,
+                                                                                   pb->nx, pb->d_errOV, 1);
+                pb->launches += 1;
+                KFP_CUDA(cudaGetLastError());
             }
             KFP_CUDA(cudaEventRecord(pb->ev[3 + 2 * g], pb->stream));
             pb->final_slab.assign(ntot, nullptr);
@@ -1798,10 +1811,9 @@ kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth) {
     }
     if (depth == pb->pipe) return KFP_OK;
     const Plan &pl = pb->plan;
-    if (depth > 1 && (pb->gauss_seidel || pb->ovrec || pb->s_begin != 0 || pb->s_end != pb->S || !pl.fused || pl.col ||
-                      pl.window || pb->pipe != 1)) {
-        set_err("kfp_swr_set_pipeline: needs the Jacobi schedule, every subdomain on this process, the per-step "
-                "cluster kernel, no overlap recording, and a fresh setup (plan: %s)", pl.text.c_str());
+    if (depth > 1 && (pb->s_begin != 0 || pb->s_end != pb->S || !pl.fused || pl.col || pl.window || pb->pipe != 1)) {
+        set_err("kfp_swr_set_pipeline: needs every subdomain on this process, the per-step cluster kernel and a "
+                "fresh setup (plan: %s)", pl.text.c_str());
         return KFP_E_INVAL;
     }
     if (depth == 1) {
@@ -1843,11 +1855,27 @@ kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth) {
         for (int ii = 0; ii < ntot; ++ii) {
             SubDev sd = pb->subs[ii];
             sd.lag = d;
-            if (d > 0)
+            if (d > 0) {
                 for (int q = 0; q < 2; ++q)
                     if (kfp_status st = swr_alloc(pb, &sd.slab[q], (size_t)(sd.hi - sd.lo + 1) * nx)) return st;
+                for (int side = 0; side < 2; ++side)  // overlap records of this slot (recording on)
+                    if (sd.ovn[side] > 0)
+                        if (kfp_status st = swr_alloc(pb, &sd.ovb[side], (size_t)sd.ovn[side] * TR)) return st;
+            }
             pb->psubs[(size_t)d * ntot + ii] = sd;
         }
+    if (pb->ovrec && pb->npairs > 0) {  // the overlap pairs of every slot, slot-major
+        std::vector<int2> pp;
+        for (int d = 0; d < D; ++d)
+            for (int r = 0; r < pb->n_rep; ++r)
+                for (int i = 0; i + 1 < nl; ++i)
+                    pp.push_back(make_int2(d * ntot + r * nl + i, d * ntot + r * nl + i + 1));
+        void *q = nullptr;
+        KFP_CUDA(cudaMalloc(&q, sizeof(int2) * pp.size()));
+        pb->d_ppairs = static_cast<int2 *>(q);
+        pb->swr_allocs.push_back(static_cast<double *>(q));
+        KFP_CUDA(cudaMemcpy(pb->d_ppairs, pp.data(), sizeof(int2) * pp.size(), cudaMemcpyHostToDevice));
+    }
     {
         void *q = nullptr;
         KFP_CUDA(cudaMalloc(&q, sizeof(SubDev) * pb->psubs.size()));
@@ -1871,7 +1899,11 @@ kfp_status kfp_swr_set_overlap_error(kfp_problem pb, int32_t on) {
         return KFP_E_STATE;
     }
     const Plan &pl = pb->plan;
-    if (on && (!pl.fused || pl.col || pl.window || pb->pipe > 1)) {
+    if (on && pb->pipe > 1 && !pb->ovrec) {
+        set_err("kfp_swr_set_overlap_error: turn the recording on before kfp_swr_set_pipeline");
+        return KFP_E_STATE;
+    }
+    if (on && (!pl.fused || pl.col || pl.window)) {
         set_err("kfp_swr_set_overlap_error: needs the per-step cluster kernel (plan: %s)", pl.text.c_str());
         return KFP_E_INVAL;
     }
@@ -1943,16 +1975,24 @@ kfp_status kfp_swr_iterate_until(kfp_problem pb, kfp_metric metric, double eps, 
         return KFP_E_STATE;
     }
     const unsigned long long *hist = metric == KFP_ERR_T ? pb->d_errT : metric == KFP_ERR_IF ? pb->d_errIF : pb->d_errOV;
-    for (int i = 0; i < k_max; ++i) {
-        if (kfp_status st = kfp_swr_iterate(pb, 1)) return st;
-        unsigned long long bits = 0;  // replica 0 (the batch's first replica)
-        KFP_CUDA(cudaMemcpyAsync(&bits, hist + (pb->k_done - 1), sizeof bits, cudaMemcpyDeviceToHost, pb->stream));
+    // pipelined: whole groups of up to `pipe` iterations, then the first of them that met the tolerance
+    const int step_iters = std::max(1, pb->pipe);
+    int done = 0, hit = -1;
+    while (done < k_max && hit < 0) {
+        const int n = std::min(step_iters, k_max - done), k0 = pb->k_done;
+        if (kfp_status st = kfp_swr_iterate(pb, n)) return st;
+        std::vector<unsigned long long> bits(n);  // replica 0 (the batch's first replica)
+        KFP_CUDA(cudaMemcpyAsync(bits.data(), hist + k0, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost,
+                                 pb->stream));
         KFP_CUDA(cudaStreamSynchronize(pb->stream));
-        double e;
-        std::memcpy(&e, &bits, 8);
-        if (!(e >= eps)) break;  // below the tolerance (or NaN: stop as well)
+        for (int i = 0; i < n && hit < 0; ++i) {
+            double e;
+            std::memcpy(&e, &bits[i], 8);
+            if (!(e >= eps)) hit = k0 + i + 1;  // below the tolerance (or NaN: stop as well)
+        }
+        done += n;
     }
-    if (k_out) *k_out = pb->k_done;
+    if (k_out) *k_out = hit > 0 ? hit : pb->k_done;
     return KFP_OK;
 }
 

@@ -33,9 +33,10 @@ RUNS = {
 }
 
 
-def _solve(kfp, run, depth, lam=None):
+def _solve(kfp, run, depth, lam=None, schedule="jacobi"):
     with kfp.Problem(ki.make_problem(run)) as pb:
         pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
+        pb.set_schedule(schedule)
         if depth > 1:
             pb.set_pipeline(depth)
         pb.reset()
@@ -49,11 +50,14 @@ def _solve(kfp, run, depth, lam=None):
                     traces=[pb.trace(i, d) for i in range(run.n_sub - 1) for d in (0, 1)], launches=pb.launch_count())
 
 
+@pytest.mark.parametrize("schedule", ["jacobi", "gauss_seidel"])
 @pytest.mark.parametrize("name", list(RUNS))
 @pytest.mark.parametrize("depth", [2, 3, 64])
-def test_pipelined_equals_unpipelined(kfp, name, depth):
+def test_pipelined_equals_unpipelined(kfp, name, depth, schedule):
+    """Jacobi: slots lag by the iteration offset; Gauss-Seidel (SWR1-SWR4): a wavefront, subdomain s of slot d
+    lagging 2 d + s steps."""
     run = RUNS[name]
-    a, b = _solve(kfp, run, 1), _solve(kfp, run, min(depth, run.K))
+    a, b = _solve(kfp, run, 1, schedule=schedule), _solve(kfp, run, min(depth, run.K), schedule=schedule)
     assert np.array_equal(a["eT"], b["eT"]) and np.array_equal(a["eI"], b["eI"]), (name, a["eI"], b["eI"])
     for x, y in zip(a["slabs"], b["slabs"]):
         assert np.array_equal(x, y), name
@@ -94,13 +98,60 @@ def test_pipeline_rejected_combinations(kfp):
     run = RUNS["c0"]
     with kfp.Problem(ki.make_problem(run)) as pb:
         pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
-        pb.set_schedule("gauss_seidel")
-        with pytest.raises(kfp.KfpError):
-            pb.set_pipeline(4)
-    with kfp.Problem(ki.make_problem(run)) as pb:
-        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
         pb.set_pipeline(4)
         with pytest.raises(kfp.KfpError):
-            pb.set_schedule("gauss_seidel")
-        with pytest.raises(kfp.KfpError):
             pb.set_overlap_error(True)
+        with pytest.raises(kfp.KfpError):
+            pb.set_pipeline(1)
+    with kfp.Problem(ki.make_problem(run)) as pb:
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        pb.reset()
+        pb.iterate(1)
+        with pytest.raises(kfp.KfpError):  # only right after setup / reset
+            pb.set_pipeline(4)
+
+
+def test_pipelined_gauss_seidel_random_traces_vs_oracle(kfp):
+    """The paper's own experiment shape (SWR1-SWR4, random lambda^0, the split-FEM scheme) through the
+    wavefront: against the oracle's Gauss-Seidel."""
+    import oracle
+
+    run = ki.Run("fem_gs", ki.Grid(64, 200, 30, 1.0, 0.3), "zero", "robin", 11.0, 3, 2, 6, q=2.5, scheme="split_fem")
+    g = run.grid
+    rng = np.random.default_rng(13)
+    lam = (rng.uniform(-1, 1, size=(1, g.nt, g.nx)), rng.uniform(-1, 1, size=(1, g.nt, g.nx)))
+    b = _solve(kfp, run, 6, lam, schedule="gauss_seidel")
+    r = oracle.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q,
+                   schedule="gauss_seidel", init_traces=lam)
+
+    def rel(x, y):
+        return float(np.abs(np.asarray(x) - y).max() / np.abs(y).max())
+
+    assert rel(b["eT"], r["err_T"]) <= 1e-9 and rel(b["eI"], r["err_if"]) <= 1e-9
+    for x, y in zip(b["slabs"], r["uT_sub"]):
+        assert rel(x, y) <= 1e-9
+
+
+@pytest.mark.parametrize("schedule", ["jacobi", "gauss_seidel"])
+def test_pipelined_overlap_error_and_tolerance_stopping(kfp, schedule):
+    """The paper's overlap quantity recorded per slot under pipelining is bitwise the unpipelined
+    one, and tolerance stopping finds the same first iteration (group-wise: it may run further)."""
+    run = ki.Run("fem_j0", ki.paper_grid(0), "zero", "robin", 11.0, 3, 2, 24, q=2.5, scheme="split_fem")
+    g = run.grid
+    lam = np.random.default_rng(21).uniform(-1, 1, size=(g.nt, g.nx))
+    out = {}
+    for depth in (1, 5):
+        with kfp.Problem(ki.make_problem(run)) as pb:
+            pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
+            pb.set_schedule(schedule)
+            pb.set_overlap_error(True)
+            if depth > 1:
+                pb.set_pipeline(depth)
+            pb.reset()
+            pb.set_initial_trace(0, 0, lam)
+            k = pb.iterate_until(1e-6, run.K)
+            out[depth] = (k, pb.overlap_history(), pb.history())
+    (k1, eo1, h1), (k5, eo5, h5) = out[1], out[5]
+    assert k1 == k5, (k1, k5)
+    n = len(eo1)
+    assert np.array_equal(eo1, eo5[:n]) and np.array_equal(h1[1], h5[1][:n])

@@ -28,6 +28,7 @@ import kfp_inputs as ki  # noqa: E402
 from paper_1306_4596_b200 import Problem  # noqa: E402
 
 EPS, KMAX = 1e-6, 150
+PIPE = 8
 PAPER = {  # Table 1 of the paper (its own FEM discretisation), for context only
     ("CSWR", 3): [70, 105, 132, ">150", ">150"], ("OSWR(p)", 3): [9, 12, 15, 17, 18], ("OSWR(p,q)", 3): [9, 10, 10, 10, 13],
     ("CSWR", 0): ["-"] * 5, ("OSWR(p)", 0): [12, 17, 20, 23, 26], ("OSWR(p,q)", 0): [11, 12, 13, 14, 16],
@@ -50,12 +51,14 @@ def run_level(j, ov, name, kind, p, q, scheme, tau_full=False, lam_lo=-1.0):
         pb.set_schedule("gauss_seidel")
         if metric == "overlap":
             pb.set_overlap_error(True)
+        if PIPE > 1 and metric == "overlap":
+            pb.set_pipeline(PIPE)  # wavefront SWR1-SWR4: bitwise the serial schedule (tests/test_gpu_pipeline.py)
         pb.reset()
         pb.set_initial_trace(0, 0, lam[0])  # lambda_1^0 (toward Omega_1's right end)
         pb.set_initial_trace(0, 1, lam[1])  # unused by SWR1-SWR4 (lambda_2^k comes from u_1^k)
         if metric == "overlap":
             k = pb.iterate_until(EPS, KMAX, "overlap")
-            hist = list(pb.overlap_history())
+            hist = list(pb.overlap_history())[:k]  # pipelined groups may run past the first k below eps
         else:  # stall detection for the non-converging classical method
             hist = []
             for k in range(1, KMAX + 1):
@@ -78,10 +81,13 @@ def main():
     ap.add_argument("--jmax", type=int, default=4)
     ap.add_argument("--tau-full", action="store_true", help="FEM: tau = Delta t instead of Delta t / 2 (reading F2)")
     ap.add_argument("--lam-unit", action="store_true", help="lambda^0 ~ U(0, 1) instead of U(-1, 1)")
+    ap.add_argument("--pipe", type=int, default=8, help="pipeline depth (FEM runs; 1 = the serial launch order)")
     a = ap.parse_args()
+    global PIPE
+    PIPE = a.pipe
     out = {"scheme": {"fem": "split_fem (the paper's, P:443-525)", "fd": "imex_fd"}[a.scheme], "eps": EPS,
            "kmax": KMAX, "schedule": "gauss_seidel (SWR1-SWR4)", "tau": "dt" if a.tau_full else "dt/2",
-           "lambda0": "U(0,1)" if a.lam_unit else "U(-1,1)", "results": {}}
+           "lambda0": "U(0,1)" if a.lam_unit else "U(-1,1)", "pipeline_depth": a.pipe, "results": {}}
     for ov in (3, 0):
         for name, kind, p, q in METHODS:
             row = []
