@@ -351,6 +351,7 @@ struct kfp_problem_s {
     unsigned long long *d_errT = nullptr, *d_errIF = nullptr;
     unsigned long long *d_errOV = nullptr;  // [n_rep][K_max] overlap differences (the paper's eq. 'error')
     bool ovrec = false;                     // overlap recording on (kfp_swr_set_overlap_error)
+    bool ov_alloc = false;                  // its buffers / pairs exist (they stay until the next setup)
     int2 *d_pairs = nullptr;                // local interfaces (left, right subdomain index) of every replica
     int npairs = 0;
     // pipelined Jacobi iterations (kfp_swr_set_pipeline): depth D, D slots of every descriptor (slot d
@@ -402,6 +403,7 @@ void free_swr(kfp_problem pb) {
     pb->d_pairs = nullptr;
     pb->npairs = 0;
     pb->ovrec = false;
+    pb->ov_alloc = false;
     pb->pipe = 1;
     pb->psubs.clear();
     pb->d_psubs = nullptr;  // (in swr_allocs)
@@ -1907,7 +1909,7 @@ kfp_status kfp_swr_set_overlap_error(kfp_problem pb, int32_t on) {
         set_err("kfp_swr_set_overlap_error: needs the per-step cluster kernel (plan: %s)", pl.text.c_str());
         return KFP_E_INVAL;
     }
-    if (!on || pb->ovrec) {
+    if (!on || pb->ov_alloc) {  // off, or back on with the buffers of an earlier call
         pb->ovrec = on != 0;
         return KFP_OK;
     }
@@ -1936,6 +1938,7 @@ kfp_status kfp_swr_set_overlap_error(kfp_problem pb, int32_t on) {
     pb->npairs = (int)pairs.size();
     KFP_CUDA(cudaMemcpy(pb->d_subs, pb->subs.data(), sizeof(SubDev) * pb->subs.size(), cudaMemcpyHostToDevice));
     pb->ovrec = true;
+    pb->ov_alloc = true;
     return KFP_OK;
 }
 
