@@ -138,9 +138,13 @@ __host__ __device__ constexpr size_t fused_smem_bytes() {
 // --------------------------------------------------------------------------- passes
 // DIR = -1: every row of the chunk has v >= 0 (upwind neighbour m-1); +1: v < 0
 // (neighbour m+1); 0: generic (per-row side, ragged length).
-template <int B, int NR, int DIR>
+// ONFLY (the cluster kernel's full chunks, DIR != 0): the transport weights come from the row index
+// instead of the table, c1 = (q/a)|nu_l| = |l dq + vbq|, c0 u + c1 nb = (q/a) u + c1 (nb - u) -- one
+// shared-memory load per row fewer (+3 % on c2); the forcing coefficients stay in the table.
+template <int B, int NR, int DIR, bool ONFLY = false>
 __device__ __forceinline__ void pass_a_reg(const double *tile_w, const double *coef_w, int lane, double q,
-                                           const double (&fx)[NR], double (&h)[B], int Lw, int jv2_0, double &hend) {
+                                           const double (&fx)[NR], double (&h)[B], int Lw, int jv2_0, double &hend,
+                                           double qa = 0.0, double vbq = 0.0, double dq = 0.0) {
     constexpr int kC = 2 + NR;
     double hp = 0.0;
 #pragma unroll
@@ -158,7 +162,13 @@ __device__ __forceinline__ void pass_a_reg(const double *tile_w, const double *c
         double f = 0.0;
 #pragma unroll
         for (int r = 0; r < NR; ++r) f = fma(c[2 + r], fx[r], f);
-        const double rp = fma(c[1], nb, fma(c[0], u, f));
+        double rp;
+        if (DIR == 0 || !ONFLY) {
+            rp = fma(c[1], nb, fma(c[0], u, f));
+        } else {
+            const double c1 = fabs(fma(static_cast<double>(l), dq, vbq));
+            rp = fma(c1, nb - u, fma(qa, u, f));
+        }
         if (DIR == 0) {
             h[l] = (l < Lw) ? fma(q, hp, rp) : 0.0;
             hend = (l == Lw - 1) ? h[l] : hend;
@@ -458,8 +468,10 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 else if (full && jv2_1 < 0) pass_a_fem<B, 1>(tile_w, lane, q, c1, c4, vb, dnu, jv2_0, h, Lw, hend, gtop, gl);
                 else pass_a_fem<B, 0>(tile_w, lane, q, c1, c4, vb, dnu, jv2_0, h, Lw, hend, gtop, gl);
             } else {
-                if (full && jv2_0 >= 0) pass_a_reg<B, NR, -1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
-                else if (full && jv2_1 < 0) pass_a_reg<B, NR, 1>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
+                // (q/a) v_j dt / h_x at the chunk's first row and its increment per row
+                const double dq = P.qa * P.hv * P.dt * P.nx, vbq = fma(static_cast<double>(jb), dq, -P.qa * (0.5 * P.nv) * P.hv * P.dt * P.nx);
+                if (full && jv2_0 >= 0) pass_a_reg<B, NR, -1, true>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend, P.qa, vbq, dq);
+                else if (full && jv2_1 < 0) pass_a_reg<B, NR, 1, true>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend, P.qa, vbq, dq);
                 else pass_a_reg<B, NR, 0>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
             }
             if (trace_cta) {  // raw r (no incoming-trace term) at the outgoing-trace rows, for the Robin trace (R11)
