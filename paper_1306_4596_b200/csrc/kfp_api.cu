@@ -888,7 +888,7 @@ kfp_status build_fused_tables(kfp_problem pb, const Plan &pl, std::vector<double
         for (int r = 0; r < pb->f_rank; ++r) c[(size_t)j * kc + 2 + r] = (double)(qa * (*fv_host)[(size_t)r * nn + j]);
     }
     const int kQ = ((pl.P * pl.B + 2) + 1) / 2 * 2;
-    std::vector<double> t(2 * kQ + 2 * pl.B, 0.0);
+    std::vector<double> t(2 * kQ + 2 * pl.B + 4, 0.0);
     const long double q = pb->q;
     long double qq = 1.0L, ss = 0.0L;
     for (int k = 0; k < kQ; ++k) {
@@ -903,6 +903,11 @@ kfp_status build_fused_tables(kfp_problem pb, const Plan &pl, std::vector<double
         t[2 * kQ + 2 * l] = (double)kap;
         t[2 * kQ + 2 * l + 1] = (double)powl(q, pl.L - l);
     }
+    // pass C of full chunks (kfp_fused.cuh): 1/q, 1/(1-q^2), q^{L+1}, q^L
+    t[2 * kQ + 2 * pl.B + 0] = (double)(1.0L / q);
+    t[2 * kQ + 2 * pl.B + 1] = (double)(1.0L / (1.0L - q * q));
+    t[2 * kQ + 2 * pl.B + 2] = (double)powl(q, pl.L + 1);
+    t[2 * kQ + 2 * pl.B + 3] = (double)powl(q, pl.L);
     void *d1 = nullptr, *d2 = nullptr;
     KFP_CUDA(cudaMalloc(&d1, sizeof(double) * c.size()));
     KFP_CUDA(cudaMemcpy(d1, c.data(), sizeof(double) * c.size(), cudaMemcpyHostToDevice));

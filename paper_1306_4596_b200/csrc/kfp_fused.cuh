@@ -110,10 +110,10 @@ struct FusedSmem {
     static constexpr int kRows = P * B;
     static constexpr int kCoef = 2 + NR;  // c0', c1', g_0' .. g_{NR-1}'
     static constexpr int kQ = fused_kq<B, P>();
-    static constexpr int kTab = 2 * kQ + 2 * B;
+    static constexpr int kTab = 2 * kQ + 2 * B + 4;  // + (1/q, 1/(1-q^2), q^{L+1}, q^L) for pass C
     alignas(128) double tile[P * kSlot];  // per warp: u^n rows [L][36] (FEM: [L+2][36], rows cr0-1 .. cr0+L)
     alignas(16) double coef[FEM ? 2 : kRows * kCoef];  // per warp: its chunk's rows of coefT
-    alignas(16) double tab[kTab];                   // qp[kQ] | s2[kQ] | kr[2B]  (copy of FusedParams::tabs)
+    alignas(16) double tab[kTab];                   // qp[kQ] | s2[kQ] | kr[2B] | ex[4]  (copy of FusedParams::tabs)
     alignas(16) double l2m[kL2M];                   // level-2 map of this (subdomain, block)
     double he[P * kCS];          // y at the chunk's last row (zero carry); then final Y carries
     double ks[P * kCS];          // k at the chunk's first row (zero carry); then final X carries
@@ -623,8 +623,16 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             double *dst = unew + static_cast<size_t>(cr0) * P.nx + m;
             const size_t pitch = P.nx;
             if (Lw == B && L == B) {
+                // kap(l, L) Y + q^{L-l} X = (c Y) q^{l+1} + (X - c q^{L+1} Y) q^{L-l}, c = 1/(1 - q^2):
+                // two running products instead of a table load per row
+                const double *ex = kr + 2 * B;  // 1/q, 1/(1-q^2), q^{L+1}, q^L
+                double A = ex[1] * Y * q, Rr = fma(-ex[1] * ex[2], Y, X) * ex[3];
 #pragma unroll
-                for (int l = 0; l < B; ++l) h[l] = fma(kr[2 * l], Y, fma(kr[2 * l + 1], X, h[l]));
+                for (int l = 0; l < B; ++l) {
+                    h[l] += A + Rr;
+                    A *= q;
+                    Rr *= ex[0];
+                }
             } else {
 #pragma unroll
                 for (int l = 0; l < B; ++l)
