@@ -144,7 +144,7 @@ __host__ __device__ constexpr size_t fused_smem_bytes() {
 template <int B, int NR, int DIR, bool ONFLY = false>
 __device__ __forceinline__ void pass_a_reg(const double *tile_w, const double *coef_w, int lane, double q,
                                            const double (&fx)[NR], double (&h)[B], int Lw, int jv2_0, double &hend,
-                                           double qa = 0.0, double vbq = 0.0, double dq = 0.0) {
+                                           double qa = 0.0, double vbq = 0.0, double dq = 0.0, int uoff = 0) {
     constexpr int kC = 2 + NR;
     double hp = 0.0;
 #pragma unroll
@@ -156,6 +156,8 @@ __device__ __forceinline__ void pass_a_reg(const double *tile_w, const double *c
         if (DIR == 0) {
             const int off = (jv2_0 + 2 * l >= 0) ? -1 : 1;  // 2j - nv >= 0: v >= 0 -> left neighbour
             nb = row[off];
+        } else if (DIR == 2) {
+            nb = row[uoff];  // the whole chunk on one side of v = 0: a warp-uniform offset
         } else {
             nb = row[DIR];
         }
@@ -470,8 +472,11 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             } else {
                 // (q/a) v_j dt / h_x at the chunk's first row and its increment per row
                 const double dq = P.qa * P.hv * P.dt * P.nx, vbq = fma(static_cast<double>(jb), dq, -P.qa * (0.5 * P.nv) * P.hv * P.dt * P.nx);
-                if (full && jv2_0 >= 0) pass_a_reg<B, NR, -1, true>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend, P.qa, vbq, dq);
-                else if (full && jv2_1 < 0) pass_a_reg<B, NR, 1, true>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend, P.qa, vbq, dq);
+                // full chunks on one side of v = 0 share one body with a warp-uniform neighbour offset (the
+                // two sign-specialised copies doubled the hot code; the kernel is instruction-cache sensitive)
+                if (full && (jv2_0 >= 0 || jv2_1 < 0))
+                    pass_a_reg<B, NR, 2, true>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend, P.qa, vbq, dq,
+                                                jv2_0 >= 0 ? -1 : 1);
                 else pass_a_reg<B, NR, 0>(tile_w, coef_w, lane, q, fx, h, Lw, jv2_0, hend);
             }
             if (trace_cta) {  // raw r (no incoming-trace term) at the outgoing-trace rows, for the Robin trace (R11)
