@@ -16,6 +16,7 @@ Rank 0 prints ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -229,16 +230,26 @@ def bench_single(args):
     traffic = committed_traffic(plan := pb.plan())
     eT, eI = pb.history()
 
-    # end to end through the public API with host buffers (create -> solve -> read back)
+    # end to end through the public API with host buffers (create -> solve -> read back): the input tables and
+    # the result live in pinned host memory (allocated outside the timed region)
     e2e_steps = max(1, min(args.steps, 2))
+
+    def pinned_copy(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        return t
+
+    pins = [pinned_copy(np.asarray(x, dtype=np.float64)) for x in (prob.ft, prob.fv, prob.fx, prob.u0v, prob.u0x)]
+    prob_pinned = dataclasses.replace(prob, **{k: t.numpy() for k, t in zip(("ft", "fv", "fx", "u0v", "u0x"), pins)})
+    uT_pinned = torch.empty((g.nv + 1, g.nx), dtype=torch.float64, pin_memory=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(stream)
     d2h = 0
     for _ in range(e2e_steps):
-        with Problem(prob, device=dev) as q:
+        with Problem(prob_pinned, device=dev) as q:
             q.set_stream(stream.cuda_stream)
-            uT = q.solve(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
+            uT = q.solve(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q, out=uT_pinned.numpy())
             h = q.history()
             d2h = uT.nbytes + h[0].nbytes + h[1].nbytes
     e1.record(stream)

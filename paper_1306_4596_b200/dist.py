@@ -36,7 +36,7 @@ class CudaBlock:
     """The local block on this rank's GPU, through the C-ABI (libkfp.so)."""
 
     def __init__(self, prob, kind: str, p: float, overlap: int, n_sub: int, K: int, rank: int, world: int,
-                 device: int, q=None):
+                 device: int, q=None, stream=None):
         from .kfp import Problem
 
         self.s_begin, self.s_end = block_of(rank, world, n_sub)
@@ -46,7 +46,7 @@ class CudaBlock:
         # a real stream made current: the library's launches, torch's NCCL exchange (which orders itself
         # after the current stream) and the timing events all sit on it (the legacy default stream, handle 0,
         # would leave the library on its own non-blocking stream, unordered with the exchange)
-        self.stream = torch.cuda.Stream(device=device)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=device)
         torch.cuda.set_stream(self.stream)
         self.pb = Problem(prob, device=device)
         self.pb.set_stream(self.stream.cuda_stream)
@@ -187,16 +187,26 @@ def bench_main(args, default_workload, clock_sampler=None, peaks=None):
     per_launch = torch.tensor([kernel_ms[0] / 1e3 / step_launches], device=dev)
     dist.all_reduce(per_launch, op=dist.ReduceOp.MAX)
     plan = blk.pb.plan()
+    ranges = [blk.pb.subdomain_range(s) for s in range(blk.s_begin, blk.s_end)]  # for the e2e output buffers
     blk.close()
 
     # end to end through the public API (host tables in, u(T) out), max over ranks
     dist.barrier()
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # input tables and results in pinned host memory (allocated outside the timed region), same stream
+    import dataclasses
+
+    pins = {k: torch.empty(np.shape(getattr(prob, k)), dtype=torch.float64, pin_memory=True)
+            for k in ("ft", "fv", "fx", "u0v", "u0x")}
+    for k, t in pins.items():
+        t.numpy()[...] = getattr(prob, k)
+    prob_pinned = dataclasses.replace(prob, **{k: t.numpy() for k, t in pins.items()})
+    outs = [torch.empty((hi - lo + 1, g.nx), dtype=torch.float64, pin_memory=True) for lo, hi in ranges]
     f0.record(stream)
-    b2 = CudaBlock(prob, run.kind, run.p, run.overlap, run.n_sub, run.K, rank, world, local)
+    b2 = CudaBlock(prob_pinned, run.kind, run.p, run.overlap, run.n_sub, run.K, rank, world, local, stream=stream)
     hist = one(b2)
-    uT = [b2.subdomain_uT(s) for s in range(b2.s_begin, b2.s_end)]
+    uT = [b2.pb.subdomain_uT(s, out=o.numpy()) for s, o in zip(range(b2.s_begin, b2.s_end), outs)]
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([f0.elapsed_time(f1)], device=dev)

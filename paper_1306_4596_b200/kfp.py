@@ -232,9 +232,13 @@ class Problem:
                                                 c(recv_right)))
 
     def solve(self, kind: str, p: float, overlap: int, n_sub: int, K: int, copy: bool = True,
-              q: Optional[float] = None):
+              q: Optional[float] = None, out: Optional[np.ndarray] = None):
+        """Setup + K iterations; returns the assembled u^K(T) (into `out`, e.g. a pinned buffer, if given)."""
         g = self.grid
-        out = np.empty((g.nv + 1, g.nx)) if copy else None
+        if out is not None:
+            assert out.dtype == np.float64 and out.flags.c_contiguous and out.size == (g.nv + 1) * g.nx
+        else:
+            out = np.empty((g.nv + 1, g.nx)) if copy else None
         if q is None:
             _check(load().kfp_swr_solve(self._h, KIND[kind], float(p), int(overlap), int(n_sub), int(K), _ptr(out)))
         else:
@@ -256,9 +260,11 @@ class Problem:
         _check(load().kfp_swr_subdomain_range(self._h, int(s), ctypes.byref(lo), ctypes.byref(hi)))
         return lo.value, hi.value
 
-    def subdomain_uT(self, s: int):
+    def subdomain_uT(self, s: int, out: Optional[np.ndarray] = None):
         lo, hi = self.subdomain_range(s)
-        out = np.empty((hi - lo + 1, self.grid.nx))
+        if out is None:
+            out = np.empty((hi - lo + 1, self.grid.nx))
+        assert out.dtype == np.float64 and out.flags.c_contiguous and out.size == (hi - lo + 1) * self.grid.nx
         _check(load().kfp_swr_subdomain_uT(self._h, int(s), _ptr(out)))
         return out
 
