@@ -101,6 +101,13 @@ bool fused_kernel(int B, int NR, int P, FusedKernel *k, size_t *smem, bool fem =
     KFP_ENTRY(8, 2, 8) KFP_ENTRY(16, 2, 8) KFP_ENTRY(17, 2, 8) KFP_ENTRY(32, 2, 8) KFP_ENTRY(33, 2, 8)
     KFP_ENTRY(8, 4, 8) KFP_ENTRY(16, 4, 8) KFP_ENTRY(17, 4, 8) KFP_ENTRY(32, 4, 8) KFP_ENTRY(33, 4, 8)
     KFP_ENTRY(32, 2, 16) KFP_ENTRY(33, 2, 16)
+    // rank-1 forcing (the c4 family): one 8-B coefficient load per row instead of a 16-B pair
+    if (!fem && !pipe && NR == 1) {
+        if (B == 32 && P == 8) { fused_entry<32, 1, 8>(k, smem); return true; }
+        if (B == 33 && P == 8) { fused_entry<33, 1, 8>(k, smem); return true; }
+        if (B == 32 && P == 16) { fused_entry<32, 1, 16>(k, smem); return true; }
+        if (B == 33 && P == 16) { fused_entry<33, 1, 16>(k, smem); return true; }
+    }
     KFP_FENTRY(8, 8) KFP_FENTRY(16, 8) KFP_FENTRY(17, 8) KFP_FENTRY(32, 8) KFP_FENTRY(33, 8)
     KFP_FENTRY(32, 16) KFP_FENTRY(33, 16)
 #undef KFP_ENTRY
@@ -253,14 +260,16 @@ Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool al
             }
         FusedKernel k;
         size_t smem = 0;
-        if (allow_fused && B > 0 && L <= 33 && f_rank <= kfp::kNRmax && fused_kernel(B, NR, P, &k, &smem, fem)) {
+        // rank <= 1 forcing takes the NR = 1 instantiation where one exists (the tables keep 4-double rows)
+        const int NRc = (f_rank <= 1 && !fem && B > 0 && fused_kernel(B, 1, P, &k, &smem)) ? 1 : NR;
+        if (allow_fused && B > 0 && L <= 33 && f_rank <= kfp::kNRmax && fused_kernel(B, NRc, P, &k, &smem, fem)) {
             pl.fused = true;
             pl.fem = fem;
             pl.P = P;
             pl.C = C;
             pl.L = L;
             pl.B = B;
-            pl.NR = NR;
+            pl.NR = NRc;
             pl.b = L;
             pl.R = P * L;
             pl.smem = smem;
@@ -877,7 +886,7 @@ kfp_status build_fused_tables(kfp_problem pb, const Plan &pl, std::vector<double
                               double **tabs, std::vector<void *> *owner) {
     *coefT = *tabs = nullptr;
     if (!pl.fused || pl.col) return KFP_OK;
-    const int kc = 2 + pl.NR, nn = pb->nv + 1;
+    const int kc = 2 + std::max(2, pl.NR), nn = pb->nv + 1;  // NR = 1 rows padded (kfp_fused.cuh kCoef)
     const long double qa = (long double)pb->q / pb->a;
     std::vector<double> c((size_t)nn * kc, 0.0);
     for (int j = 0; j < nn; ++j) {
@@ -1827,6 +1836,7 @@ kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth) {
         set_err("kfp_swr_set_pipeline: a pipelined setup cannot go back to depth 1; set it up again");
         return KFP_E_INVAL;
     }
+    if (pb->plan.NR == 1) pb->plan.NR = 2;  // no pipelined NR = 1 variants: same table rows, zero 2nd coefficient
     {
         FusedKernel k;
         size_t smem = 0;

@@ -108,7 +108,7 @@ struct FusedSmem {
     static constexpr int kTileRows = B + (FEM ? 2 : 0);
     static constexpr int kSlot = slot_doubles<kTileRows>();
     static constexpr int kRows = P * B;
-    static constexpr int kCoef = 2 + NR;  // c0', c1', g_0' .. g_{NR-1}'
+    static constexpr int kCoef = 2 + (NR < 2 ? 2 : NR);  // c0', c1', g_0' .. g_{NR-1}' (rows padded to 4)
     static constexpr int kQ = fused_kq<B, P>();
     static constexpr int kTab = 2 * kQ + 2 * B + 4;  // + (1/q, 1/(1-q^2), q^{L+1}, q^L) for pass C
     alignas(128) double tile[P * kSlot];  // per warp: u^n rows [L][36] (FEM: [L+2][36], rows cr0-1 .. cr0+L)
@@ -145,7 +145,7 @@ template <int B, int NR, int DIR, bool ONFLY = false>
 __device__ __forceinline__ void pass_a_reg(const double *tile_w, const double *coef_w, int lane, double q,
                                            const double (&fx)[NR], double (&h)[B], int Lw, int jv2_0, double &hend,
                                            double qa = 0.0, double vbq = 0.0, double dq = 0.0, int uoff = 0) {
-    constexpr int kC = 2 + NR;
+    constexpr int kC = 2 + (NR < 2 ? 2 : NR);  // the table's row stride (NR = 1 rows padded to 4 doubles)
     double hp = 0.0;
 #pragma unroll
     for (int l = 0; l < B; ++l) {
