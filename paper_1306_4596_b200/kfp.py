@@ -235,8 +235,8 @@ class Problem:
               q: Optional[float] = None, out: Optional[np.ndarray] = None):
         """Setup + K iterations; returns the assembled u^K(T) (into `out`, e.g. a pinned buffer, if given)."""
         g = self.grid
-        if out is not None:
-            assert out.dtype == np.float64 and out.flags.c_contiguous and out.size == (g.nv + 1) * g.nx
+        if out is not None and not (out.dtype == np.float64 and out.flags.c_contiguous and out.size == (g.nv + 1) * g.nx):
+            raise ValueError("solve: out must be a C-contiguous float64 array of (nv+1)*nx elements")
         else:
             out = np.empty((g.nv + 1, g.nx)) if copy else None
         if q is None:
@@ -264,7 +264,8 @@ class Problem:
         lo, hi = self.subdomain_range(s)
         if out is None:
             out = np.empty((hi - lo + 1, self.grid.nx))
-        assert out.dtype == np.float64 and out.flags.c_contiguous and out.size == (hi - lo + 1) * self.grid.nx
+        if not (out.dtype == np.float64 and out.flags.c_contiguous and out.size == (hi - lo + 1) * self.grid.nx):
+            raise ValueError("subdomain_uT: out must be a C-contiguous float64 array of the slab's size")
         _check(load().kfp_swr_subdomain_uT(self._h, int(s), _ptr(out)))
         return out
 

@@ -83,6 +83,21 @@ def test_split_fem_validation_without_device(lib):
     assert e.value.status == kfp.KFP_E_CFL
 
 
+def test_out_buffers_are_checked_before_any_call(lib):
+    """kfp.Problem.solve(out=...) rejects a wrong-sized or non-contiguous buffer in Python (the C-ABI would write
+    (nv+1)*nx doubles through the pointer)."""
+    import numpy as np
+
+    from paper_1306_4596_b200 import kfp
+
+    pb = kfp.Problem.__new__(kfp.Problem)  # no device needed: the check precedes every library call
+    pb.grid = type("G", (), {"nv": 4, "nx": 8})()
+    with pytest.raises(ValueError):
+        pb.solve("robin", 1.0, 0, 2, 1, out=np.zeros((5, 7)))
+    with pytest.raises(ValueError):
+        pb.solve("robin", 1.0, 0, 2, 1, out=np.zeros((8, 5)).T)
+
+
 def test_product_path_does_not_import_oracle():
     """The product package never imports the oracle (and vice versa)."""
     pkg = os.path.join(ROOT, "paper_1306_4596_b200")
