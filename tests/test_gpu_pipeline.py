@@ -155,3 +155,31 @@ def test_pipelined_overlap_error_and_tolerance_stopping(kfp, schedule):
     assert k1 == k5, (k1, k5)
     n = len(eo1)
     assert np.array_equal(eo1, eo5[:n]) and np.array_equal(h1[1], h5[1][:n])
+
+
+@pytest.mark.parametrize("schedule", ["jacobi", "gauss_seidel"])
+def test_pipelined_batched_sweep_equals_unpipelined(kfp, schedule):
+    """A batched Robin-parameter sweep (replicas with their own (p, q)) through the pipeline, with overlap
+    recording: every replica's err_T, err_if, err_ov and slabs bitwise the unpipelined batch's."""
+    run = ki.Run("fem_b", ki.Grid(64, 200, 24, 1.0, 0.24), "zero", "robin", 4.0, 3, 2, 7, scheme="split_fem")
+    g = run.grid
+    lam = np.random.default_rng(31).uniform(-1, 1, size=(g.nt, g.nx))
+    ps, qs = [1.0, 4.23, 11.0], [1.0, 4.23, 2.5]
+    res = {}
+    for depth in (1, 4):
+        with kfp.Problem(ki.make_problem(run)) as pb:
+            pb.setup_batch("robin", ps, run.overlap, run.n_sub, run.K, qs=qs)
+            pb.set_schedule(schedule)
+            pb.set_overlap_error(True)
+            if depth > 1:
+                pb.set_pipeline(depth)
+            pb.reset()
+            pb.set_initial_trace(0, 0, lam)
+            pb.iterate(run.K)
+            res[depth] = [(pb.batch_history(r), pb.overlap_history(r), [pb.batch_subdomain_uT(r, s) for s in range(2)])
+                          for r in range(len(ps))]
+    for r in range(len(ps)):
+        (h1, o1, u1), (h4, o4, u4) = res[1][r], res[4][r]
+        assert np.array_equal(h1[0], h4[0]) and np.array_equal(h1[1], h4[1]) and np.array_equal(o1, o4), r
+        for a, b in zip(u1, u4):
+            assert np.array_equal(a, b), r
