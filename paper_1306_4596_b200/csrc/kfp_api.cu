@@ -639,7 +639,8 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
         pb->launches += 1;
     } else {
         kfp::step_phase1<<<dim3(pl.C, ntiles, nsub), block, pl.smem, pb->stream>>>(P);
-        kfp::step_phase2<<<dim3((pb->nx + 127) / 128, 1, nsub), 128, 0, pb->stream>>>(P);
+        // phase 2: a warp per column (block recurrences as shuffle scans; step_phase2 is the serial reference form)
+        kfp::step_phase2_warp<<<dim3((pb->nx + 3) / 4, 1, nsub), 128, 0, pb->stream>>>(P);
         kfp::step_phase3<<<dim3(pl.C, ntiles, nsub), block, pl.smem, pb->stream>>>(P);
         pb->launches += 3;
     }

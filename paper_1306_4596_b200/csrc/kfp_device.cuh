@@ -749,6 +749,105 @@ __global__ void step_phase2(const StepParams P) {
     }
 }
 
+// General path, phase 2, warp per column: the same algebra as step_phase2, with the block recurrences
+//   Y_{c+1} = q^{R_c} Y_c + F_c            (forward, Y_0 given)
+//   X_c     = q^{R_c} X_{c+1} + kap(0, R_c) Y_c + G_c   (backward, X_nblk given)
+// evaluated as affine scans over the blocks: lane i owns a segment of ceil(nblk / 32) consecutive blocks,
+// composes its segment's affine map, a Kogge-Stone shuffle scan gives every segment its incoming value,
+// and the lane replays its segment.  Two sweeps: zero carries (for the Woodbury end terms), then the
+// final carries.  For tall columns (many blocks) this replaces a serial per-thread chain.
+__device__ __forceinline__ void p2w_sweep(const StepParams &P, int sub, int m, int lane, int nblk, int n, double yinit,
+                                          double xinit, bool final_pass, double (&yb)[4], double (&xb)[4]) {
+    const int per = (nblk + kWarp - 1) / kWarp, c0 = min(nblk, lane * per), c1 = min(nblk, c0 + per);
+    const int brow[4] = {0, 1, n - 2, n - 1};
+    auto Bv = [&](int c, int slot) { return P.blkagg[((static_cast<size_t>(sub) * P.C + c) * 8 + slot) * P.nx + m]; };
+    auto Rc = [&](int c) { return min(P.R, n - c * P.R); };
+    double *car = P.carry + static_cast<size_t>(sub) * P.C * 2 * P.nx + m;  // [c][2][nx]
+    // forward: segment map, inclusive scan (lower lanes first), exclusive incoming value
+    double a = 1.0, b = 0.0;
+    for (int c = c0; c < c1; ++c) {
+        const double qr = P.qp[Rc(c)];
+        a *= qr;
+        b = fma(qr, b, Bv(c, 0));
+    }
+    for (int d = 1; d < kWarp; d <<= 1) {
+        const double au = __shfl_up_sync(0xffffffffu, a, d), bu = __shfl_up_sync(0xffffffffu, b, d);
+        if (lane >= d) {
+            b = fma(a, bu, b);
+            a *= au;
+        }
+    }
+    double ain = __shfl_up_sync(0xffffffffu, a, 1), bin = __shfl_up_sync(0xffffffffu, b, 1);
+    if (lane == 0) {
+        ain = 1.0;
+        bin = 0.0;
+    }
+    double Y = fma(ain, yinit, bin);
+    for (int c = c0; c < c1; ++c) {
+        for (int q = 0; q < 4; ++q)
+            if (brow[q] / P.R == c) yb[q] = Y;
+        car[(static_cast<size_t>(c) * 2 + 0) * P.nx] = Y;
+        Y = fma(P.qp[Rc(c)], Y, Bv(c, 0));
+    }
+    // backward: segment map over (c1-1 .. c0), scan from the high lanes, incoming value from lane + 1
+    a = 1.0;
+    b = 0.0;
+    for (int c = c1 - 1; c >= c0; --c) {
+        const double qr = P.qp[Rc(c)];
+        const double Yc = car[(static_cast<size_t>(c) * 2 + 0) * P.nx];
+        a *= qr;
+        b = fma(qr, b, fma(kapf(P.qp, P.s2, 0, Rc(c)), Yc, Bv(c, 1)));
+    }
+    for (int d = 1; d < kWarp; d <<= 1) {
+        const double ad = __shfl_down_sync(0xffffffffu, a, d), bd = __shfl_down_sync(0xffffffffu, b, d);
+        if (lane + d < kWarp) {
+            b = fma(a, bd, b);
+            a *= ad;
+        }
+    }
+    double aout = __shfl_down_sync(0xffffffffu, a, 1), bout = __shfl_down_sync(0xffffffffu, b, 1);
+    if (lane == kWarp - 1) {
+        aout = 1.0;
+        bout = 0.0;
+    }
+    double X = fma(aout, xinit, bout);
+    for (int c = c1 - 1; c >= c0; --c) {
+        for (int q = 0; q < 4; ++q)
+            if (brow[q] / P.R == c) xb[q] = X;
+        if (final_pass) car[(static_cast<size_t>(c) * 2 + 1) * P.nx] = X;
+        const double Yc = car[(static_cast<size_t>(c) * 2 + 0) * P.nx];
+        X = fma(P.qp[Rc(c)], X, fma(kapf(P.qp, P.s2, 0, Rc(c)), Yc, Bv(c, 1)));
+    }
+    // the block-boundary captures live on the lane owning that block: broadcast them
+    for (int q = 0; q < 4; ++q) {
+        const int owner = per > 0 ? min(kWarp - 1, (brow[q] / P.R) / per) : 0;
+        yb[q] = __shfl_sync(0xffffffffu, yb[q], owner);
+        xb[q] = __shfl_sync(0xffffffffu, xb[q], owner);
+    }
+}
+
+__global__ void __launch_bounds__(128) step_phase2_warp(const StepParams P) {
+    const int lane = threadIdx.x & 31, m = blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+    const int sub = blockIdx.z;
+    if (m >= P.nx) return;  // a whole warp per column
+    const SubDev &S = P.subs[sub];
+    const int nblk = S.nblk, n = S.n;
+    const int brow[4] = {0, 1, n - 2, n - 1};
+    auto Bv = [&](int c, int slot) { return P.blkagg[((static_cast<size_t>(sub) * P.C + c) * 8 + slot) * P.nx + m]; };
+    auto Rc = [&](int c) { return min(P.R, n - c * P.R); };
+    double yb[4] = {0, 0, 0, 0}, xb[4] = {0, 0, 0, 0}, xt[4];
+    p2w_sweep(P, sub, m, lane, nblk, n, 0.0, 0.0, false, yb, xb);  // zero block carries
+    for (int q = 0; q < 4; ++q) {
+        const int c = brow[q] / P.R, l = brow[q] - c * P.R, R = Rc(c);
+        xt[q] = Bv(c, 2 + q) + kapf(P.qp, P.s2, l, R) * yb[q] + P.qp[R - l] * xb[q];
+    }
+    const double s0 = S.wt0 * xt[0] + S.wt1 * xt[1];
+    const double s1 = S.wb0 * xt[2] + S.wb1 * xt[3];
+    const double c0 = S.Mi00 * s0 + S.Mi01 * s1;
+    const double c1 = S.Mi10 * s0 + S.Mi11 * s1;
+    p2w_sweep(P, sub, m, lane, nblk, n, -c0 / P.a, -c1 / P.a, true, yb, xb);  // the final carries
+}
+
 // General path, phase 3: reload k, level 1 with the block carries, pass C.
 __global__ void __launch_bounds__(kMaxWarps * kWarp) step_phase3(const StepParams P) {
     extern __shared__ __align__(128) char smraw[];
