@@ -183,3 +183,34 @@ def test_pipelined_batched_sweep_equals_unpipelined(kfp, schedule):
         assert np.array_equal(h1[0], h4[0]) and np.array_equal(h1[1], h4[1]) and np.array_equal(o1, o4), r
         for a, b in zip(u1, u4):
             assert np.array_equal(a, b), r
+
+
+def test_api_error_paths(kfp):
+    """The documented error codes of the newer calls (include/kfp.h): wrong call order -> KFP_E_STATE, bad
+    arguments -> KFP_E_INVAL; the handle stays usable afterwards."""
+    run = RUNS["c0"].with_(K=4)
+    with kfp.Problem(ki.make_problem(run)) as pb:
+        with pytest.raises(kfp.KfpError) as e:  # before any setup
+            pb.set_overlap_error(True)
+        assert e.value.status == kfp.KFP_E_STATE
+        with pytest.raises(kfp.KfpError) as e:
+            pb.set_pipeline(2)
+        assert e.value.status == kfp.KFP_E_STATE
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        with pytest.raises(kfp.KfpError) as e:  # overlap history with the recording off
+            pb.reset()
+            pb.iterate(1)
+            pb.overlap_history()
+        assert e.value.status == kfp.KFP_E_STATE
+        with pytest.raises(kfp.KfpError) as e:  # KFP_ERR_OVERLAP without recording
+            pb.iterate_until(1e-6, 2, "overlap")
+        assert e.value.status == kfp.KFP_E_STATE
+        with pytest.raises(kfp.KfpError) as e:  # beyond K_max
+            pb.iterate_until(1e-6, run.K, "err_if")
+        assert e.value.status == kfp.KFP_E_STATE
+        with pytest.raises(kfp.KfpError) as e:
+            pb.set_pipeline(0)
+        assert e.value.status == kfp.KFP_E_INVAL
+        pb.reset()  # still usable
+        k = pb.iterate_until(0.0, run.K, "err_T")  # eps = 0: never met, runs K_max
+        assert k == run.K and len(pb.history()[0]) == run.K
