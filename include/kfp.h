@@ -51,7 +51,8 @@ typedef enum {
     KFP_E_CFL = -2,    /* Vmax * dt / h_x > 1: the upwind step would not be a convex combination */
     KFP_E_NOMEM = -3,  /* device allocation failed */
     KFP_E_CUDA = -4,   /* CUDA runtime error or no usable device */
-    KFP_E_STATE = -6   /* call order (e.g. history before any solve) */
+    KFP_E_STATE = -6,  /* call order (e.g. history before any solve) */
+    KFP_E_NONFINITE = -7 /* an iteration's error is NaN or infinite (the solve blew up; failure detection) */
 } kfp_status;
 
 typedef enum {
@@ -209,7 +210,9 @@ kfp_status kfp_swr_setup_batch(kfp_problem pb, kfp_kind kind, const double *ps, 
 kfp_status kfp_swr_batch_history(kfp_problem pb, int32_t rep, int32_t cap, int32_t *K_out, double *err_T,
                                  double *err_if);
 
-/* u^k(T) of subdomain s (0 <= s < n_sub) of replica rep, host [(hi_s - lo_s + 1) * nx]. */
+/* u^k(T) of subdomain s (0 <= s < n_sub) of replica rep, host [(hi_s - lo_s + 1) * nx].  KFP_E_INVAL for a
+ * bad rep / s or a setup that does not hold every subdomain (s_begin > 0 or s_end < n_sub); KFP_E_STATE
+ * before the first iteration after a setup / reset. */
 kfp_status kfp_swr_batch_subdomain_uT(kfp_problem pb, int32_t rep, int32_t s, double *out);
 
 /* kfp_swr_solve with OSWR(p, q) (see kfp_swr_setup_pq). */
@@ -259,9 +262,10 @@ kfp_status kfp_swr_overlap_history(kfp_problem pb, int32_t rep, int32_t cap, int
  * kfp_last_timing reports per-group windows. */
 kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth);
 
-/* Tolerance stopping: run iterations until `metric` of one of them (replica 0) is below eps
- * (or not finite), or k_max more iterations have run; *k_out = the first iteration (counted since the
- * last reset) that met the tolerance, else the iterations done.  Unpipelined: one iteration at a time,
+/* Tolerance stopping: run iterations until `metric` of one of them (replica 0) is below eps,
+ * or k_max more iterations have run; *k_out = the first iteration (counted since the last reset) that met
+ * the tolerance, else the iterations done.  A NaN / infinite error (every error reduction propagates NaN)
+ * stops at once and returns KFP_E_NONFINITE with *k_out = that iteration.  Unpipelined: one iteration at a time,
  * one stream synchronisation each (8 bytes read).  Pipelined (kfp_swr_set_pipeline): whole groups of
  * up to depth iterations, so up to depth - 1 iterations beyond *k_out may have run (kfp_error_history
  * and the solution reflect all that ran).  KFP_E_STATE if k_done + k_max > K_max or KFP_ERR_OVERLAP
@@ -269,7 +273,8 @@ kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth);
 kfp_status kfp_swr_iterate_until(kfp_problem pb, kfp_metric metric, double eps, int32_t k_max, int32_t *k_out);
 
 /* Copy the local subdomain s's current u_s(T) slab [(hi_s-lo_s+1)*nx] to host
- * memory (s is the global subdomain index, s_begin <= s < s_end). */
+ * memory (s is the global subdomain index, s_begin <= s < s_end).  KFP_E_STATE before the first
+ * iteration after a setup / reset (the slab would be stale). */
 kfp_status kfp_swr_subdomain_uT(kfp_problem pb, int32_t s, double *out);
 
 /* Node range of global subdomain s under the current setup. */

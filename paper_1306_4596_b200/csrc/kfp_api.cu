@@ -22,8 +22,6 @@
 #include "../../include/kfp.h"
 #include "kfp_device.cuh"
 #include "kfp_fused.cuh"
-#include "kfp_window.cuh"
-#include "kfp_col.cuh"
 
 using kfp::SubDev;
 using kfp::StepParams;
@@ -51,8 +49,6 @@ void set_err(const char *fmt, ...) {
     } while (0)
 
 struct Plan {
-    bool col = false;    // cluster-free column-tile kernel (kfp_col.cuh): 8 columns x the whole column per CTA
-    bool window = false; // persistent pipelined window kernel (one launch per SWR iteration); implies fused geometry
     bool fused = false;  // fused TMA/cluster kernel; else the three-phase path
     bool fem = false;    // the split-FEM instantiation of the fused kernel
     int P = 8, b = 32, R = 256, C = 1;
@@ -66,14 +62,6 @@ struct Plan {
 struct FusedData {
     CUtensorMap *maps = nullptr;  // [2][nsub][2]: load maps then store maps
     double *l2c = nullptr, *coefT = nullptr, *tabs = nullptr;
-    // window kernel
-    double *cfn = nullptr;               // [nt][kMaxRank] dt ft_r(t_{n+1})
-    unsigned int *flags = nullptr;       // [nsub][ntiles][C] step flags
-    unsigned int *fault = nullptr;       // watchdog word
-    // column-tile kernel
-    double *ctab = nullptr;              // [nsub][NC][kCT] chunk constants
-    double *ctabs = nullptr;             // qp | s2 | kr of the column kernel
-    double *fvq = nullptr;               // [nv+1][NR] (q/a) fv_r(j)
 };
 
 using FusedKernel = void (*)(const kfp::FusedParams);
@@ -116,135 +104,19 @@ bool fused_kernel(int B, int NR, int P, FusedKernel *k, size_t *smem, bool fem =
 }
 constexpr int kBs[] = {8, 16, 17, 32, 33};
 
-using WindowKernel = void (*)(const kfp::WinParams);
-template <int B, int NR, int P>
-void window_entry(WindowKernel *k, size_t *smem) {
-    *k = kfp::step_window<B, NR, P>;
-    *smem = kfp::window_smem_bytes<B, NR, P>();
-}
-// instantiated (B, NR, P) combinations of the window kernel (P = 16 warps, 1 CTA per SM)
-bool window_kernel(int B, int NR, int P, WindowKernel *k, size_t *smem) {
-#define KFP_WENTRY(BB, NN, PP)             \
-    if (B == BB && NR == NN && P == PP) {  \
-        window_entry<BB, NN, PP>(k, smem); \
-        return true;                       \
-    }
-    KFP_WENTRY(8, 2, 8) KFP_WENTRY(16, 2, 8) KFP_WENTRY(17, 2, 8) KFP_WENTRY(32, 2, 8) KFP_WENTRY(33, 2, 8)
-    KFP_WENTRY(8, 4, 8) KFP_WENTRY(16, 4, 8) KFP_WENTRY(17, 4, 8) KFP_WENTRY(32, 4, 8) KFP_WENTRY(33, 4, 8)
-#undef KFP_WENTRY
-    return false;
-}
-constexpr int kWBs[] = {8, 16, 17, 32, 33};
-
-using ColKernel = void (*)(const kfp::ColParams);
-template <int B, int NR, int P>
-void col_entry(ColKernel *k, size_t *smem) {
-    *k = kfp::step_col<B, NR, P>;
-    *smem = kfp::col_smem_bytes<B, NR, P>();
-}
-// instantiated (B, NR, P) combinations of the column-tile kernel
-bool col_kernel(int B, int NR, int P, ColKernel *k, size_t *smem) {
-#define KFP_CENTRY(BB, NN, PP)          \
-    if (B == BB && NR == NN && P == PP) { \
-        col_entry<BB, NN, PP>(k, smem);   \
-        return true;                      \
-    }
-    KFP_CENTRY(8, 2, 8) KFP_CENTRY(16, 2, 8) KFP_CENTRY(17, 2, 8) KFP_CENTRY(32, 2, 8) KFP_CENTRY(33, 2, 8)
-    KFP_CENTRY(8, 2, 16) KFP_CENTRY(16, 2, 16) KFP_CENTRY(17, 2, 16) KFP_CENTRY(32, 2, 16) KFP_CENTRY(33, 2, 16)
-#undef KFP_CENTRY
-    return false;
-}
-
 // Launch geometry for columns of at most n_max unknown rows.
 // Fused path: P = 16 warps per CTA, chunks of L rows (target 17), row blocks of
 // R = 16 L rows, C = ceil(n_max / R) <= 8 CTAs per cluster.  Otherwise the
 // three-phase path (P = 8, b = 32, block aggregates through global memory).
-Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool allow_window = false, int nx = 0,
-               bool allow_col = true, bool fem = false) {
+Plan make_plan(const std::vector<int> &ns, int f_rank, bool allow_fused, bool fem = false) {
     Plan pl;
-    if (fem) allow_window = allow_col = false;  // the split-FEM scheme exists only in the per-step cluster kernel
     const int n_max = *std::max_element(ns.begin(), ns.end());
     const int NR = (f_rank <= 2) ? 2 : 4;
-    // Column-tile kernel (opt-in, KFP_COL=1; correct, but measured slower than the cluster kernel on c2
-    // and c4): 8-column tiles, the whole column in one CTA of P = 8 (2 CTAs per SM,
-    // n <= 1056) or 16 warps (n <= 2112), chunks of L <= 33 rows.
-    if (allow_col && allow_fused && nx > 0 && nx % kfp::kColW == 0 && NR == 2 && getenv("KFP_COL") && !getenv("KFP_WINDOW") &&
-        n_max <= 4 * 16 * 33 && (int)ns.size() <= kfp::kColMaxSub) {
-        const int P = (n_max <= 4 * 8 * 33) ? 8 : 16;
-        int L = (n_max + 4 * P - 1) / (4 * P);
-        if (L % 2 == 0 && L < 33) ++L;  // odd: the 4 chunks of a warp alternate smem bank halves (64-B rows)
-        int B = 0;
-        for (int bb : kBs)
-            if (bb >= L) {
-                B = bb;
-                break;
-            }
-        ColKernel k;
-        size_t smem = 0;
-        if (B > 0 && col_kernel(B, NR, P, &k, &smem)) {
-            pl.col = pl.fused = true;
-            pl.P = P;
-            pl.C = 1;
-            pl.L = L;
-            pl.B = B;
-            pl.NR = NR;
-            pl.b = L;
-            pl.R = 4 * P * L;
-            pl.smem = smem;
-            char buf[200];
-            snprintf(buf, sizeof buf, "column-tile P=%d L=%d (B=%d) NC=%d W=8 NR=%d smem=%zu", P, L, B, 4 * P, NR, smem);
-            pl.text = buf;
-            return pl;
-        }
-    }
-    // Window kernel (SWR iterations): P = 8 warps (1 CTA per SM, 255 registers: two tiles' rows in
-    // registers), chunks of L <= 33 rows, C <= 8 CTAs per cluster.
-    // Opt-in (KFP_WINDOW=1): correct, but measured slower than the per-step kernel on c2.
-    if (allow_window && allow_fused && getenv("KFP_WINDOW") && !getenv("KFP_NO_WINDOW") && f_rank <= kfp::kNRmax) {
-        const int P = 8;
-        int C = 1;
-        while (C < 8 && (n_max + P * C - 1) / (P * C) > 33) ++C;
-        int L = (n_max + P * C - 1) / (P * C);
-        for (bool ok = false; !ok && L <= 33;) {
-            ok = true;
-            for (int n : ns)
-                if (n % (P * L) == 1) ok = false;
-            if (!ok) ++L;
-        }
-        int B = 0;
-        for (int bb : kWBs)
-            if (bb >= L) {
-                B = bb;
-                break;
-            }
-        WindowKernel k;
-        size_t smem = 0;
-        if (B > 0 && L <= 33 && window_kernel(B, NR, P, &k, &smem)) {
-            pl.window = pl.fused = true;
-            pl.P = P;
-            pl.C = C;
-            pl.L = L;
-            pl.B = B;
-            pl.NR = NR;
-            pl.b = L;
-            pl.R = P * L;
-            pl.smem = smem;
-            char buf[200];
-            snprintf(buf, sizeof buf, "window-pipelined P=%d L=%d (B=%d) R=%d C=%d NR=%d smem=%zu", P, L, B, pl.R, C, NR,
-                     smem);
-            pl.text = buf;
-            return pl;
-        }
-    }
     // P = 8 warps (2 CTAs per SM) first, then P = 16 (1 CTA per SM): the smallest cluster whose
     // warps hold at most 33 rows; the column's first/last row blocks must hold >= 2 rows.
-    const char *force = getenv("KFP_FORCE_P");  // debugging / experiments only
-    const char *forceC = getenv("KFP_FORCE_C");  // debugging / experiments only
     for (int P : {8, 16}) {
-        if (force && atoi(force) != P) continue;
         int C = 1;
         while (C < 8 && (n_max + P * C - 1) / (P * C) > 33) ++C;
-        if (forceC && atoi(forceC) >= C && atoi(forceC) <= 8) C = atoi(forceC);
         int L = (n_max + P * C - 1) / (P * C);
         for (bool ok = false; !ok && L <= 33;) {
             ok = true;
@@ -380,7 +252,6 @@ struct kfp_problem_s {
     double *edge_sendR[2] = {nullptr, nullptr}, *edge_recvR[2] = {nullptr, nullptr};
     std::vector<double *> zero_on_reset;  // parity-0 incoming buffers
 
-    unsigned int epoch = 0;  // window kernel: base of the step-flag values of the next launch
     int64_t launches = 0;
     std::vector<cudaEvent_t> ev;  // 2 per iteration of the last iterate call + 2 around it
     int ev_used = 0;
@@ -535,6 +406,9 @@ StepParams base_params(kfp_problem pb) {
     P.q = pb->q;
     P.a = pb->a;
     P.qa = pb->q / pb->a;
+#ifdef KFP_MUTATE  // test-only mutant build (libkfp_mut.so): one step-kernel coefficient off by 1e-3
+    P.qa *= 1.0 + 1e-3;
+#endif
     P.hv = pb->hv;
     P.dt = pb->dt;
     P.dnu = pb->dnu;
@@ -568,41 +442,6 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
     P.C = pl.C;
     const int ntiles = (pb->nx + kfp::kWarp - 1) / kfp::kWarp;
     const dim3 block(pl.P * kfp::kWarp);
-    if (pl.window) {
-        set_err("launch_step: the window plan has no per-step kernel");
-        return KFP_E_STATE;
-    }
-    if (pl.col) {
-        kfp::ColParams CP;
-        CP.S = P;
-        CP.tmaps = fd.maps;
-        CP.fvq = fd.fvq;
-        CP.ctab = fd.ctab;
-        CP.tabs = fd.ctabs;
-        CP.rec_rows = rec_rows;
-        CP.nrec = nrec;
-        CP.L = pl.L;
-        CP.ntiles = pb->nx / kfp::kColW;
-        CP.nsub = nsub;
-        CP.qdn = pb->q / pb->a * (pb->hv * pb->dt / pb->hx);
-        ColKernel k;
-        size_t smem;
-        col_kernel(pl.B, pl.NR, pl.P, &k, &smem);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(std::max(1, std::min(pl.Gc_total, nsub * CP.ntiles)));
-        cfg.blockDim = block;
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = pb->stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        KFP_CUDA(cudaLaunchKernelEx(&cfg, k, CP));
-        pb->launches += 1;
-        KFP_CUDA(cudaGetLastError());
-        return KFP_OK;
-    }
     if (pl.fused) {
         kfp::FusedParams FP;
         FP.S = P;
@@ -648,166 +487,6 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
     return KFP_OK;
 }
 
-// One persistent launch of the window kernel: steps [n0, n1) of every local subdomain.
-kfp_status launch_window(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, const FusedData &fd, int n0, int n1) {
-    P.P = pl.P;
-    P.b = pl.b;
-    P.R = pl.R;
-    P.C = pl.C;
-    const int ntiles = (pb->nx + kfp::kWarp - 1) / kfp::kWarp;
-    kfp::WinParams W;
-    W.S = P;
-    W.tmaps = fd.maps;
-    W.l2m = fd.l2c;
-    W.coefT = fd.coefT;
-    W.tabs = fd.tabs;
-    W.cfn = fd.cfn;
-    W.flags = fd.flags;
-    W.fault = fd.fault;
-    W.L = pl.L;
-    W.ntiles = ntiles;
-    W.nsub = nsub;
-    W.n0 = n0;
-    W.n1 = n1;
-    int G = std::min(pl.Gc_total, nsub * ntiles);
-    if (const char *e = getenv("KFP_WIN_G")) G = std::max(1, std::min(G, atoi(e)));  // experiments only (<= resident)
-    W.G = G;
-    W.epoch = pb->epoch;
-    W.dbg = getenv("KFP_WIN_DBG") ? atoi(getenv("KFP_WIN_DBG")) : 0;  // experiments only
-    pb->epoch += (unsigned int)pb->nt + 1u;
-    WindowKernel k;
-    size_t smem;
-    window_kernel(pl.B, pl.NR, pl.P, &k, &smem);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(pl.C, G, 1);
-    cfg.blockDim = dim3(pl.P * kfp::kWarp);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = pb->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = pl.C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    KFP_CUDA(cudaLaunchKernelEx(&cfg, k, W));
-    pb->launches += 1;
-    KFP_CUDA(cudaGetLastError());
-    return KFP_OK;
-}
-
-// Window-kernel tables: dt ft_r(t_{n+1}) per step, zeroed step flags, watchdog word.
-kfp_status build_window_tables(kfp_problem pb, const Plan &pl, int nsub, FusedData *fd, std::vector<void *> *owner) {
-    if (!pl.window) return KFP_OK;
-    const int nt = pb->nt, ntiles = (pb->nx + kfp::kWarp - 1) / kfp::kWarp;
-    std::vector<double> cfn((size_t)nt * kfp::kMaxRank, 0.0);
-    for (int n = 0; n < nt; ++n)
-        for (int r = 0; r < pb->f_rank; ++r)  // the same product launch_step forms on the host
-            cfn[(size_t)n * kfp::kMaxRank + r] = pb->dt * pb->ft[(size_t)r * (nt + 1) + n + 1];
-    void *d1 = nullptr, *d2 = nullptr, *d3 = nullptr;
-    const size_t nflags = (size_t)nsub * ntiles * pl.C;
-    KFP_CUDA(cudaMalloc(&d1, sizeof(double) * cfn.size()));
-    owner->push_back(d1);
-    KFP_CUDA(cudaMemcpy(d1, cfn.data(), sizeof(double) * cfn.size(), cudaMemcpyHostToDevice));
-    KFP_CUDA(cudaMalloc(&d2, sizeof(unsigned int) * nflags));
-    owner->push_back(d2);
-    KFP_CUDA(cudaMemset(d2, 0, sizeof(unsigned int) * nflags));
-    KFP_CUDA(cudaMalloc(&d3, 16));
-    owner->push_back(d3);
-    KFP_CUDA(cudaMemset(d3, 0, 16));
-    fd->cfn = static_cast<double *>(d1);
-    fd->flags = static_cast<unsigned int *>(d2);
-    fd->fault = static_cast<unsigned int *>(d3);
-    pb->epoch = 0;
-    return KFP_OK;
-}
-
-// Column-tile kernel tables: tensor maps (box 8 x 4L), per-subdomain chunk constants
-// (q^{L_k}, kap(0, L_k), q^{s_k}, kap(e_k, n), q^{n-e_k}), qp | s2 | kr, and (q/a) fv_r(j).
-kfp_status build_col_tables(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, FusedData *fd,
-                            std::vector<void *> *owner) {
-    if (!pl.col) return KFP_OK;
-    const long double q = pb->q;
-    auto qpw = [&](long double e) { return powl(q, e); };
-    auto s2f = [&](int k) {  // sum_{t<k} q^{2t}
-        long double sacc = 0, t = 1;
-        for (int i = 0; i < k; ++i) {
-            sacc += t;
-            t *= q * q;
-        }
-        return sacc;
-    };
-    auto kap = [&](int r, int len) { return qpw(r + 1) * s2f(len - r); };
-    const size_t ns = subs.size();
-    const int NC = 4 * pl.P, L = pl.L;
-    // tensor maps
-    std::vector<CUtensorMap> maps(2 * ns);
-    for (size_t i = 0; i < ns; ++i)
-        for (int qq = 0; qq < 2; ++qq) {
-            double *base = subs[i].slab[qq] + (size_t)(subs[i].first - subs[i].lo) * pb->nx;
-            if (!make_tmap(&maps[2 * i + qq], base, pb->nx, subs[i].n, 2 * L, kfp::kColW)) {
-                set_err("cuTensorMapEncodeTiled failed (column tile, nx=%d rows=%d)", pb->nx, subs[i].n);
-                return KFP_E_CUDA;
-            }
-        }
-    // chunk constants
-    std::vector<double> ct(ns * NC * kfp::kCT, 0.0);
-    for (size_t i = 0; i < ns; ++i) {
-        const int n = subs[i].n;
-        for (int k = 0; k < NC; ++k) {
-            double *e = ct.data() + (i * NC + k) * kfp::kCT;
-            const int Lk = std::max(0, std::min(L, n - k * L)), sk = k * L, ek = sk + Lk;
-            if (Lk == 0) {
-                e[0] = 1.0;
-                continue;
-            }
-            e[0] = (double)qpw(Lk);
-            e[1] = (double)kap(0, Lk);
-            e[2] = (double)qpw(sk);
-            e[3] = (ek >= n) ? 0.0 : (double)kap(ek, n);
-            e[4] = (double)qpw(n - ek);
-        }
-    }
-    // qp | s2 | kr
-    const int kQ = ((pl.B + 2) + 1) / 2 * 2;
-    std::vector<double> t(2 * kQ + 2 * pl.B, 0.0);
-    {
-        long double qq = 1.0L, ss = 0.0L;
-        for (int k = 0; k < kQ; ++k) {
-            t[k] = (double)qq;
-            t[kQ + k] = (double)ss;
-            ss += qq * qq;
-            qq *= q;
-        }
-        for (int l = 0; l < L; ++l) {
-            t[2 * kQ + 2 * l] = (double)kap(l, L);
-            t[2 * kQ + 2 * l + 1] = (double)qpw(L - l);
-        }
-    }
-    // (q/a) fv_r(j), NR columns
-    const int nn = pb->nv + 1;
-    const long double qa = (long double)pb->q / pb->a;
-    std::vector<double> fv((size_t)nn * pl.NR, 0.0);
-    for (int j = 0; j < nn; ++j)
-        for (int r = 0; r < std::min(pb->f_rank, pl.NR); ++r) fv[(size_t)j * pl.NR + r] = (double)(qa * pb->fv_host[(size_t)r * nn + j]);
-    auto up = [&](const void *src, size_t bytes, void **dst) -> kfp_status {
-        KFP_CUDA(cudaMalloc(dst, bytes));
-        owner->push_back(*dst);
-        KFP_CUDA(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
-        return KFP_OK;
-    };
-    void *d1 = nullptr, *d2 = nullptr, *d3 = nullptr, *d4 = nullptr;
-    if (kfp_status st = up(maps.data(), sizeof(CUtensorMap) * maps.size(), &d1)) return st;
-    if (kfp_status st = up(ct.data(), sizeof(double) * ct.size(), &d2)) return st;
-    if (kfp_status st = up(t.data(), sizeof(double) * t.size(), &d3)) return st;
-    if (kfp_status st = up(fv.data(), sizeof(double) * (fv.size() + 2), &d4)) return st;  // +2: 16-B bulk-copy tail
-    fd->maps = static_cast<CUtensorMap *>(d1);
-    fd->ctab = static_cast<double *>(d2);
-    fd->ctabs = static_cast<double *>(d3);
-    fd->fvq = static_cast<double *>(d4);
-    return KFP_OK;
-}
-
 // Level-2 linear maps (kfp_fused.cuh, kL2M layout): for every subdomain and row block
 // `me`, the block carries (Y_blk(me), X_blk(me)) as linear functions of the 22 inputs
 // v = (F_0..7, G_0..7, x~ at rows 0,1,n-2,n-1, g_lo, g_hi), obtained by running the
@@ -815,7 +494,7 @@ kfp_status build_col_tables(kfp_problem pb, const Plan &pl, const std::vector<Su
 kfp_status build_l2m(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, double **out,
                      std::vector<void *> *owner) {
     *out = nullptr;
-    if (!pl.fused || pl.col) return KFP_OK;
+    if (!pl.fused) return KFP_OK;
     const long double q = pb->q, a = pb->a;
     auto qp = [&](long double e) { return powl(q, e); };
     auto s2 = [&](int k) {  // sum_{t<k} q^{2t}
@@ -886,7 +565,7 @@ kfp_status build_l2m(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &
 kfp_status build_fused_tables(kfp_problem pb, const Plan &pl, std::vector<double> *fv_host, double **coefT,
                               double **tabs, std::vector<void *> *owner) {
     *coefT = *tabs = nullptr;
-    if (!pl.fused || pl.col) return KFP_OK;
+    if (!pl.fused) return KFP_OK;
     const int kc = 2 + std::max(2, pl.NR), nn = pb->nv + 1;  // NR = 1 rows padded (kfp_fused.cuh kCoef)
     const long double qa = (long double)pb->q / pb->a;
     std::vector<double> c((size_t)nn * kc, 0.0);
@@ -935,7 +614,7 @@ kfp_status build_fused_tables(kfp_problem pb, const Plan &pl, std::vector<double
 kfp_status build_tmaps(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &subs, CUtensorMap **out,
                        std::vector<void *> *owner) {
     *out = nullptr;
-    if (!pl.fused || pl.col) return KFP_OK;
+    if (!pl.fused) return KFP_OK;
     const size_t ns = subs.size();
     std::vector<CUtensorMap> maps(4 * ns);
     for (size_t i = 0; i < ns; ++i)
@@ -960,46 +639,7 @@ kfp_status build_tmaps(kfp_problem pb, const Plan &pl, const std::vector<SubDev>
 }
 
 kfp_status configure_kernels(Plan &pl) {
-    if (pl.col) {
-        ColKernel k;
-        size_t smem;
-        col_kernel(pl.B, pl.NR, pl.P, &k, &smem);
-        KFP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per_sm = 0, dev = 0, sms = 0;
-        KFP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, pl.P * kfp::kWarp, smem));
-        KFP_CUDA(cudaGetDevice(&dev));
-        KFP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (per_sm < 1) {
-            set_err("column kernel: no CTA of %d threads with %zu B smem fits on an SM", pl.P * kfp::kWarp, smem);
-            return KFP_E_CUDA;
-        }
-        pl.Gc_total = per_sm * sms;
-        return KFP_OK;
-    }
-    if (pl.window) {
-        WindowKernel k;
-        size_t smem;
-        window_kernel(pl.B, pl.NR, pl.P, &k, &smem);
-        KFP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(pl.C, 1024, 1);
-        cfg.blockDim = dim3(pl.P * kfp::kWarp);
-        cfg.dynamicSmemBytes = smem;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = pl.C;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int ncl = 0;
-        KFP_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
-        if (ncl < 1) {
-            set_err("window kernel: no cluster of %d CTAs (%zu B smem) fits on the device", pl.C, smem);
-            return KFP_E_CUDA;
-        }
-        pl.Gc_total = ncl;
-    } else if (pl.fused) {
+    if (pl.fused) {
         FusedKernel k;
         size_t smem;
         fused_kernel(pl.B, pl.NR, pl.P, &k, &smem, pl.fem);
@@ -1099,7 +739,7 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     sd.slab[0] = pb->d_mono[0];
     sd.slab[1] = pb->d_mono[1];
     woodbury(pb, sd, 0.0, 0.0);
-    Plan pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true, false, pb->nx, true, fem);
+    Plan pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true, fem);
     if (fem && !pl.fused) {
         set_err("monodomain: the split-FEM scheme needs the cluster kernel (column of %d rows > %d)", sd.n, 8 * 16 * 33);
         return KFP_E_INVAL;
@@ -1126,7 +766,6 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     if (!st) st = build_tmaps(pb, pl, std::vector<SubDev>{sd}, &fd.maps, &tmp2);
     if (!st) st = build_l2m(pb, pl, std::vector<SubDev>{sd}, &fd.l2c, &tmp2);
     if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &fd.coefT, &fd.tabs, &tmp2);
-    if (!st) st = build_col_tables(pb, pl, std::vector<SubDev>{sd}, &fd, &tmp2);
     if (!st && !rec_rows.empty()) {
         if (cudaMalloc(&d_rec, sizeof(int) * rec_rows.size()) != cudaSuccess ||
             cudaMemcpy(d_rec, rec_rows.data(), sizeof(int) * rec_rows.size(), cudaMemcpyHostToDevice) != cudaSuccess)
@@ -1462,7 +1101,7 @@ kfp_status swr_setup_impl(kfp_problem pb, kfp_kind kind, const double *ps, const
     std::vector<int> ns;
     for (const SubDev &sd : pb->subs) ns.push_back(sd.n);
     const bool fem = pb->scheme == KFP_SCHEME_SPLIT_FEM;
-    pb->plan = make_plan(ns, pb->f_rank, true, n_rep == 1, pb->nx, n_rep == 1, fem);
+    pb->plan = make_plan(ns, pb->f_rank, true, fem);
     Plan &pl = pb->plan;
     if (fem && !pl.fused) {
         set_err("kfp_swr_setup: the split-FEM scheme needs the cluster kernel (column of %d rows > %d)", n_max,
@@ -1555,8 +1194,6 @@ kfp_status swr_setup_impl(kfp_problem pb, kfp_kind kind, const double *ps, const
         kfp_status st = build_tmaps(pb, pl, pb->subs, &pb->fd.maps, &own);
         if (!st) st = build_l2m(pb, pl, pb->subs, &pb->fd.l2c, &own);
         if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &pb->fd.coefT, &pb->fd.tabs, &own);
-        if (!st) st = build_window_tables(pb, pl, ntot, &pb->fd, &own);
-        if (!st) st = build_col_tables(pb, pl, pb->subs, &pb->fd, &own);
         for (void *q : own) pb->swr_allocs.push_back(static_cast<double *>(q));
         if (st) return st;
     }
@@ -1607,9 +1244,18 @@ kfp_status kfp_swr_batch_history(kfp_problem pb, int32_t rep, int32_t cap, int32
 }
 
 kfp_status kfp_swr_batch_subdomain_uT(kfp_problem pb, int32_t rep, int32_t s, double *out) {
-    if (!pb || !pb->setup || rep < 0 || rep >= pb->n_rep || s < 0 || s >= pb->S || pb->k_done == 0 || !out) {
-        set_err("kfp_swr_batch_subdomain_uT: bad replica/subdomain or no iteration");
+    if (!pb || !pb->setup || rep < 0 || rep >= pb->n_rep || s < 0 || s >= pb->S || !out) {
+        set_err("kfp_swr_batch_subdomain_uT: bad replica/subdomain");
         return KFP_E_INVAL;
+    }
+    if (pb->s_begin != 0 || pb->s_end != pb->S) {  // replicas exist only for setups that hold every subdomain
+        set_err("kfp_swr_batch_subdomain_uT: the setup holds subdomains [%d, %d) of %d, not a batch", pb->s_begin,
+                pb->s_end, pb->S);
+        return KFP_E_INVAL;
+    }
+    if (pb->k_done == 0) {
+        set_err("kfp_swr_batch_subdomain_uT: no iteration since the setup / reset");
+        return KFP_E_STATE;
     }
     const SubDev &sd = pb->subs[(size_t)rep * pb->S + s];
     KFP_CUDA(cudaMemcpyAsync(out, final_slab(pb, (size_t)rep * pb->S + s), sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
@@ -1661,7 +1307,7 @@ kfp_status kfp_swr_set_schedule(kfp_problem pb, kfp_schedule schedule) {
         set_err("kfp_swr_set_schedule: unknown schedule %d", (int)schedule);
         return KFP_E_INVAL;
     }
-    if (schedule == KFP_GAUSS_SEIDEL && (pb->s_begin != 0 || pb->s_end != pb->S || pb->plan.window)) {
+    if (schedule == KFP_GAUSS_SEIDEL && (pb->s_begin != 0 || pb->s_end != pb->S)) {
         set_err("kfp_swr_set_schedule: Gauss-Seidel needs every subdomain on this process and a per-step plan");
         return KFP_E_INVAL;
     }
@@ -1781,14 +1427,11 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
                 FusedData fs = pb->fd;  // the tables of subdomain s
                 if (fs.maps) fs.maps += 2 * s;
                 if (fs.l2c) fs.l2c += (size_t)s * pl.C * kfp::kL2M;
-                if (fs.ctab) fs.ctab += (size_t)s * 4 * pl.P * kfp::kCT;
                 for (int n = 0; n < pb->nt; ++n) {
                     Ps.last = (n + 1 == pb->nt);  // (the cluster kernel tests its own step; see StepParams)
                     if (kfp_status st = launch_step(pb, pl, Ps, 1, n, fs)) return st;
                 }
             }
-        } else if (pb->plan.window) {
-            if (kfp_status st = launch_window(pb, pb->plan, P, nloc, pb->fd, 0, pb->nt)) return st;
         } else {
             for (int n = 0; n < pb->nt; ++n) {
                 P.last = (n + 1 == pb->nt);
@@ -1828,7 +1471,7 @@ kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth) {
     }
     if (depth == pb->pipe) return KFP_OK;
     const Plan &pl = pb->plan;
-    if (depth > 1 && (pb->s_begin != 0 || pb->s_end != pb->S || !pl.fused || pl.col || pl.window || pb->pipe != 1)) {
+    if (depth > 1 && (pb->s_begin != 0 || pb->s_end != pb->S || !pl.fused || pb->pipe != 1)) {
         set_err("kfp_swr_set_pipeline: needs every subdomain on this process, the per-step cluster kernel and a "
                 "fresh setup (plan: %s)", pl.text.c_str());
         return KFP_E_INVAL;
@@ -1837,12 +1480,15 @@ kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth) {
         set_err("kfp_swr_set_pipeline: a pipelined setup cannot go back to depth 1; set it up again");
         return KFP_E_INVAL;
     }
-    if (pb->plan.NR == 1) pb->plan.NR = 2;  // no pipelined NR = 1 variants: same table rows, zero 2nd coefficient
+    // everything below is built on copies and committed only at the end: a failed call leaves the
+    // problem as it was (include/kfp.h: state unchanged on error)
+    Plan npl = pb->plan;
+    if (npl.NR == 1) npl.NR = 2;  // no pipelined NR = 1 variants: same table rows, zero 2nd coefficient
     {
         FusedKernel k;
         size_t smem = 0;
-        if (!fused_kernel(pl.B, pl.NR, pl.P, &k, &smem, pl.fem, true)) {
-            set_err("kfp_swr_set_pipeline: no pipelined kernel variant for this plan (%s)", pl.text.c_str());
+        if (!fused_kernel(npl.B, npl.NR, npl.P, &k, &smem, npl.fem, true)) {
+            set_err("kfp_swr_set_pipeline: no pipelined kernel variant for this plan (%s)", npl.text.c_str());
             return KFP_E_INVAL;
         }
         KFP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1851,62 +1497,87 @@ kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth) {
     KFP_CUDA(cudaStreamSynchronize(pb->stream));
     const int D = depth, R = D + 1, ntot = (int)pb->subs.size(), nl = pb->s_end - pb->s_begin;
     const size_t nx = pb->nx, TR = (size_t)pb->nt * nx;
+    std::vector<double *> fresh;  // this call's allocations (freed if it fails)
+    auto al = [&](double **p, size_t count) -> kfp_status {
+        void *q = nullptr;
+        if (cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            set_err("kfp_swr_set_pipeline: device allocation of %zu doubles failed", count);
+            return KFP_E_NOMEM;
+        }
+        fresh.push_back(static_cast<double *>(q));
+        *p = static_cast<double *>(q);
+        return KFP_OK;
+    };
+    auto fail = [&](kfp_status st) {
+        for (double *p : fresh) cudaFree(p);
+        return st;
+    };
     // trace rings: slots 0 and 1 are the setup's parity buffers (slot 0 is what reset / set_initial_trace write)
-    pb->ringL.assign((size_t)pb->n_rep * (nl - 1), std::vector<double *>(R, nullptr));
-    pb->ringR.assign((size_t)pb->n_rep * (nl - 1), std::vector<double *>(R, nullptr));
+    std::vector<std::vector<double *>> ringL((size_t)pb->n_rep * (nl - 1), std::vector<double *>(R, nullptr));
+    std::vector<std::vector<double *>> ringR = ringL;
     for (int r = 0; r < pb->n_rep; ++r)
         for (int i = 0; i + 1 < nl; ++i) {
             const SubDev &left = pb->subs[(size_t)r * nl + i];
-            auto &rl = pb->ringL[(size_t)r * (nl - 1) + i], &rr = pb->ringR[(size_t)r * (nl - 1) + i];
+            auto &rl = ringL[(size_t)r * (nl - 1) + i], &rr = ringR[(size_t)r * (nl - 1) + i];
             for (int q = 0; q < 2; ++q) {
                 rl[q] = const_cast<double *>(left.gR[q]);
                 rr[q] = left.sendR[q];
             }
             for (int q = 2; q < R; ++q) {
-                if (kfp_status st = swr_alloc(pb, &rl[q], TR)) return st;
-                if (kfp_status st = swr_alloc(pb, &rr[q], TR)) return st;
+                if (kfp_status st = al(&rl[q], TR)) return fail(st);
+                if (kfp_status st = al(&rr[q], TR)) return fail(st);
             }
         }
     // slot descriptors: slot 0 = the setup's subdomains; slots d > 0 get their own slabs
-    pb->psubs.assign((size_t)D * ntot, SubDev());
+    std::vector<SubDev> psubs((size_t)D * ntot, SubDev());
     for (int d = 0; d < D; ++d)
         for (int ii = 0; ii < ntot; ++ii) {
             SubDev sd = pb->subs[ii];
             sd.lag = d;
             if (d > 0) {
                 for (int q = 0; q < 2; ++q)
-                    if (kfp_status st = swr_alloc(pb, &sd.slab[q], (size_t)(sd.hi - sd.lo + 1) * nx)) return st;
+                    if (kfp_status st = al(&sd.slab[q], (size_t)(sd.hi - sd.lo + 1) * nx)) return fail(st);
                 for (int side = 0; side < 2; ++side)  // overlap records of this slot (recording on)
                     if (sd.ovn[side] > 0)
-                        if (kfp_status st = swr_alloc(pb, &sd.ovb[side], (size_t)sd.ovn[side] * TR)) return st;
+                        if (kfp_status st = al(&sd.ovb[side], (size_t)sd.ovn[side] * TR)) return fail(st);
             }
-            pb->psubs[(size_t)d * ntot + ii] = sd;
+            psubs[(size_t)d * ntot + ii] = sd;
         }
+    int2 *d_ppairs = nullptr;
     if (pb->ovrec && pb->npairs > 0) {  // the overlap pairs of every slot, slot-major
         std::vector<int2> pp;
         for (int d = 0; d < D; ++d)
             for (int r = 0; r < pb->n_rep; ++r)
                 for (int i = 0; i + 1 < nl; ++i)
                     pp.push_back(make_int2(d * ntot + r * nl + i, d * ntot + r * nl + i + 1));
-        void *q = nullptr;
-        KFP_CUDA(cudaMalloc(&q, sizeof(int2) * pp.size()));
-        pb->d_ppairs = static_cast<int2 *>(q);
-        pb->swr_allocs.push_back(static_cast<double *>(q));
-        KFP_CUDA(cudaMemcpy(pb->d_ppairs, pp.data(), sizeof(int2) * pp.size(), cudaMemcpyHostToDevice));
+        double *q = nullptr;
+        if (kfp_status st = al(&q, (sizeof(int2) * pp.size() + 7) / 8)) return fail(st);
+        d_ppairs = reinterpret_cast<int2 *>(q);
+        if (cudaMemcpy(d_ppairs, pp.data(), sizeof(int2) * pp.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+            return fail(KFP_E_CUDA);
     }
+    FusedData pfd;
+    double *d_psubs_raw = nullptr;
+    if (kfp_status st = al(&d_psubs_raw, (sizeof(SubDev) * psubs.size() + 7) / 8)) return fail(st);
     {
-        void *q = nullptr;
-        KFP_CUDA(cudaMalloc(&q, sizeof(SubDev) * pb->psubs.size()));
-        pb->d_psubs = static_cast<SubDev *>(q);
-        pb->swr_allocs.push_back(static_cast<double *>(q));
         std::vector<void *> own;
-        kfp_status st = build_tmaps(pb, pl, pb->psubs, &pb->pfd.maps, &own);
-        if (!st) st = build_l2m(pb, pl, pb->psubs, &pb->pfd.l2c, &own);
-        for (void *o : own) pb->swr_allocs.push_back(static_cast<double *>(o));
-        if (st) return st;
-        pb->pfd.coefT = pb->fd.coefT;
-        pb->pfd.tabs = pb->fd.tabs;
+        kfp_status st = build_tmaps(pb, npl, psubs, &pfd.maps, &own);
+        if (!st) st = build_l2m(pb, npl, psubs, &pfd.l2c, &own);
+        for (void *o : own) fresh.push_back(static_cast<double *>(o));
+        if (st) return fail(st);
+        pfd.coefT = pb->fd.coefT;
+        pfd.tabs = pb->fd.tabs;
     }
+    // commit
+    pb->plan.NR = npl.NR;
+    pb->ringL = std::move(ringL);
+    pb->ringR = std::move(ringR);
+    pb->psubs = std::move(psubs);
+    pb->d_psubs = reinterpret_cast<SubDev *>(d_psubs_raw);
+    if (d_ppairs) pb->d_ppairs = d_ppairs;
+    pb->pfd = pfd;
+    pb->swr_allocs.insert(pb->swr_allocs.end(), fresh.begin(), fresh.end());
     pb->pipe = D;
     return KFP_OK;
 }
@@ -1921,7 +1592,7 @@ kfp_status kfp_swr_set_overlap_error(kfp_problem pb, int32_t on) {
         set_err("kfp_swr_set_overlap_error: turn the recording on before kfp_swr_set_pipeline");
         return KFP_E_STATE;
     }
-    if (on && (!pl.fused || pl.col || pl.window)) {
+    if (on && (!pl.fused)) {
         set_err("kfp_swr_set_overlap_error: needs the per-step cluster kernel (plan: %s)", pl.text.c_str());
         return KFP_E_INVAL;
     }
@@ -1997,6 +1668,7 @@ kfp_status kfp_swr_iterate_until(kfp_problem pb, kfp_metric metric, double eps, 
     // pipelined: whole groups of up to `pipe` iterations, then the first of them that met the tolerance
     const int step_iters = std::max(1, pb->pipe);
     int done = 0, hit = -1;
+    bool bad = false;
     while (done < k_max && hit < 0) {
         const int n = std::min(step_iters, k_max - done), k0 = pb->k_done;
         if (kfp_status st = kfp_swr_iterate(pb, n)) return st;
@@ -2007,11 +1679,20 @@ kfp_status kfp_swr_iterate_until(kfp_problem pb, kfp_metric metric, double eps, 
         for (int i = 0; i < n && hit < 0; ++i) {
             double e;
             std::memcpy(&e, &bits[i], 8);
-            if (!(e >= eps)) hit = k0 + i + 1;  // below the tolerance (or NaN: stop as well)
+            if (!std::isfinite(e)) {  // the solve blew up (failure detection)
+                hit = k0 + i + 1;
+                bad = true;
+            } else if (e < eps) {
+                hit = k0 + i + 1;
+            }
         }
         done += n;
     }
     if (k_out) *k_out = hit > 0 ? hit : pb->k_done;
+    if (bad) {
+        set_err("kfp_swr_iterate_until: iteration %d has a non-finite error", hit);
+        return KFP_E_NONFINITE;
+    }
     return KFP_OK;
 }
 
@@ -2130,6 +1811,10 @@ kfp_status kfp_swr_subdomain_uT(kfp_problem pb, int32_t s, double *out) {
         set_err("kfp_swr_subdomain_uT: subdomain %d not local", s);
         return KFP_E_INVAL;
     }
+    if (pb->k_done == 0) {
+        set_err("kfp_swr_subdomain_uT: no iteration since the setup / reset");
+        return KFP_E_STATE;
+    }
     const SubDev &sd = pb->subs[s - pb->s_begin];
     KFP_CUDA(cudaMemcpyAsync(out, final_slab(pb, s - pb->s_begin), sizeof(double) * (size_t)(sd.hi - sd.lo + 1) * pb->nx,
                              cudaMemcpyDeviceToHost, pb->stream));
@@ -2157,21 +1842,6 @@ kfp_status kfp_swr_trace(kfp_problem pb, int32_t i, int32_t dir, double *out) {
 int64_t kfp_launch_count(kfp_problem pb) { return pb ? pb->launches : -1; }
 
 #ifdef KFP_TRACE
-// debug builds only: one traced SWR iteration (window plans) -> per-CTA accumulated phase times [cta][64]
-extern "C" int kfp_debug_trace_window(kfp_problem pb, unsigned long long *host, int cap) {
-    unsigned long long *d = nullptr;
-    cudaMalloc(&d, sizeof(unsigned long long) * cap * 64);
-    cudaMemset(d, 0, sizeof(unsigned long long) * cap * 64);
-    cudaMemcpyToSymbol(kfp::g_kfp_trace, &d, sizeof(d));
-    kfp_swr_reset(pb);
-    kfp_swr_iterate(pb, 1);
-    cudaDeviceSynchronize();
-    unsigned long long *z = nullptr;
-    cudaMemcpyToSymbol(kfp::g_kfp_trace, &z, sizeof(z));
-    cudaMemcpy(host, d, sizeof(unsigned long long) * cap * 64, cudaMemcpyDeviceToHost);
-    cudaFree(d);
-    return (int)cudaGetLastError();
-}
 // debug builds only (not part of include/kfp.h): one traced step launch of the current setup
 extern "C" int kfp_debug_trace_step(kfp_problem pb, int n, unsigned long long *host, int cap) {
     unsigned long long *d = nullptr;

@@ -157,12 +157,18 @@ __device__ __forceinline__ void st_cs(double *p, double v) {  // streaming store
     asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 __device__ __forceinline__ void atomic_max_pos(unsigned long long *addr, double v) {
-    // v >= 0: the IEEE bit pattern orders like an unsigned integer.
+    // v >= 0 or NaN: the IEEE bit pattern orders like an unsigned integer, and every NaN pattern
+    // (|v| of a NaN: 0x7ff8...) is above +inf, so a NaN error survives the reduction.
     atomicMax(addr, static_cast<unsigned long long>(__double_as_longlong(v)));
 }
+// max that propagates NaN from either side (fmax drops it: a solve that blew up must not report
+// a finite error)
+__device__ __forceinline__ double nmax(double a, double b) { return (a > b || a != a) ? a : b; }
+// an error worth an atomic: positive, or NaN
+__device__ __forceinline__ bool err_pos(double v) { return !(v <= 0.0); }
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = nmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 
@@ -301,9 +307,9 @@ __device__ __forceinline__ void pass_a(const StepParams &P, const Tile &t, doubl
                 S.sendL[P.par_out][static_cast<size_t>(P.n) * P.nx + t.m] = g;
             if (S.ltype == END_DIRI && active) {
                 if (S.ifL >= 0)
-                    err_if = fmax(err_if, fabs(g - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + t.m]));
+                    err_if = nmax(err_if, fabs(g - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + t.m]));
                 if (P.last) {
-                    err_t = fmax(err_t, fabs(g - P.UT[static_cast<size_t>(S.lo) * P.nx + t.m]));
+                    err_t = nmax(err_t, fabs(g - P.UT[static_cast<size_t>(S.lo) * P.nx + t.m]));
                     unew_slab[t.m] = g;
                 }
             }
@@ -315,9 +321,9 @@ __device__ __forceinline__ void pass_a(const StepParams &P, const Tile &t, doubl
                 S.sendR[P.par_out][static_cast<size_t>(P.n) * P.nx + t.m] = g;
             if (S.rtype == END_DIRI && active) {
                 if (S.ifR >= 0)
-                    err_if = fmax(err_if, fabs(g - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + t.m]));
+                    err_if = nmax(err_if, fabs(g - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + t.m]));
                 if (P.last) {
-                    err_t = fmax(err_t, fabs(g - P.UT[static_cast<size_t>(S.hi) * P.nx + t.m]));
+                    err_t = nmax(err_t, fabs(g - P.UT[static_cast<size_t>(S.hi) * P.nx + t.m]));
                     unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + t.m] = g;
                 }
             }
@@ -488,11 +494,11 @@ __device__ __forceinline__ void pass_c(const StepParams &P, const Tile &t, const
         const int j = S.first + i;
         const double x = tile[(t.r0 + l) * kWarp + t.lane] + kapf(P.qp, P.s2, l, t.L) * Y + P.qp[t.L - l] * X;
         if (active) st_cs(unew_rows + static_cast<size_t>(i) * P.nx + t.m, x);
-        if (P.last && active) err_t = fmax(err_t, fabs(x - P.UT[static_cast<size_t>(j) * P.nx + t.m]));
+        if (P.last && active) err_t = nmax(err_t, fabs(x - P.UT[static_cast<size_t>(j) * P.nx + t.m]));
         if (active && i == 0 && S.ltype == END_ROBIN && S.ifL >= 0)
-            err_if = fmax(err_if, fabs(x - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + t.m]));
+            err_if = nmax(err_if, fabs(x - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + P.n) * P.nx + t.m]));
         if (active && i == S.n - 1 && S.rtype == END_ROBIN && S.ifR >= 0)
-            err_if = fmax(err_if, fabs(x - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + t.m]));
+            err_if = nmax(err_if, fabs(x - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + P.n) * P.nx + t.m]));
         if (S.iL_tr >= 0) {
             if (i == S.iL_tr) xtr[0 * kWarp + t.lane] = x;
             if (i == S.iL_tr + 1) xtr[1 * kWarp + t.lane] = x;
@@ -577,75 +583,16 @@ __device__ __forceinline__ void block_err_flush(const StepParams &P, const Tile 
     if (threadIdx.x == 0) {
         double a = 0.0, b = 0.0;
         for (int w = 0; w < P.P; ++w) {
-            a = fmax(a, sm.red[w]);
-            b = fmax(b, sm.red[kMaxWarps + w]);
+            a = nmax(a, sm.red[w]);
+            b = nmax(b, sm.red[kMaxWarps + w]);
         }
         const size_t go = static_cast<size_t>(t.sd->grp) * P.err_stride;
-        if (a > 0.0 && P.errIF) atomic_max_pos(P.errIF + go, a);
-        if (b > 0.0 && P.errT) atomic_max_pos(P.errT + go, b);
+        if (err_pos(a) && P.errIF) atomic_max_pos(P.errIF + go, a);
+        if (err_pos(b) && P.errT) atomic_max_pos(P.errT + go, b);
     }
 }
 
 // ------------------------------------------------------------------ kernels
-
-// Fused step: one cluster of C CTAs owns a 32-column tile of one subdomain;
-// CTA `blockIdx.x` (= cluster rank) owns row block blockIdx.x.  Block
-// aggregates are exchanged through distributed shared memory.
-__global__ void __launch_bounds__(kMaxWarps * kWarp) step_fused(const StepParams P) {
-    extern __shared__ __align__(128) char smraw[];
-    cg::cluster_group cluster = cg::this_cluster();
-    const int blk = static_cast<int>(cluster.block_rank());
-    Tile t = make_tile(P, blk);
-    Smem sm = carve(smraw, P.R, P.P);
-    const SubDev &S = *t.sd;
-    const double *uold = S.slab[P.n & 1] + static_cast<size_t>(S.first - S.lo) * P.nx;
-    double *unew_slab = S.slab[(P.n + 1) & 1];
-    double *unew = unew_slab + static_cast<size_t>(S.first - S.lo) * P.nx;
-
-    if (t.lane == 0 && t.warp < P.P) mbar_init(&sm.bar[t.warp], 1);
-    fence_mbar_init();
-    __syncwarp();
-    if (!P.from_u0 && t.warp < P.P) load_chunk(P, t, uold, sm.tile, &sm.bar[t.warp]);
-
-    double eif = 0.0, et = 0.0, hend = 0.0, kst = 0.0;
-    if (t.warp < P.P && t.L > 0) {
-        if (!P.from_u0) mbar_wait(&sm.bar[t.warp], 0);
-        pass_a(P, t, sm.tile, uold, unew_slab, sm.rtr, eif, et, hend);
-        kst = pass_b(P, t, sm.tile);
-    }
-    if (t.warp < P.P) {
-        sm.he[t.warp * kWarp + t.lane] = hend;
-        sm.ks[t.warp * kWarp + t.lane] = kst;
-    }
-    __syncthreads();
-    if (t.warp == 0) {
-        BlockAgg g = level1_zero(P, t, sm.tile, sm.he, sm.ks, sm.Y0, sm.X0);
-        sm.pub[0 * kWarp + t.lane] = g.F;
-        sm.pub[1 * kWarp + t.lane] = g.G;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) sm.pub[(2 + q) * kWarp + t.lane] = g.ab[q];
-    }
-    cluster.sync();  // publish block aggregates to the cluster
-    const int nblk = S.nblk;
-    if (t.warp == 0 && blk < nblk) {
-        const int lane = t.lane;
-        auto Fn = [&](int c) { return cluster.map_shared_rank(sm.pub, c)[0 * kWarp + lane]; };
-        auto Gn = [&](int c) { return cluster.map_shared_rank(sm.pub, c)[1 * kWarp + lane]; };
-        const int n = S.n;
-        const int brow[4] = {0, 1, n - 2, n - 1};
-        auto Ab = [&](int q) { return cluster.map_shared_rank(sm.pub, brow[q] / P.R)[(2 + q) * kWarp + lane]; };
-        double Yme, Xme;
-        level2(P, S, nblk, blk, Fn, Gn, Ab, Yme, Xme);
-        level1_carry(P, t, sm.he, sm.ks, Yme, Xme, sm.Y0, sm.X0);
-    }
-    cluster_arrive();  // our DSMEM reads are done
-    __syncthreads();
-    if (t.warp < P.P && t.L > 0) pass_c(P, t, sm.tile, sm.Y0[t.warp * kWarp + t.lane], sm.X0[t.warp * kWarp + t.lane], unew, sm.xtr, eif, et);
-    __syncthreads();
-    if (t.warp == 0 && blk < nblk) write_traces(P, t, sm.rtr, sm.xtr);
-    block_err_flush(P, t, sm, eif, et);
-    cluster_wait();  // nobody leaves while a peer may still read our pub[]
-}
 
 // General path, phase 1: passes A and B on one row block; the scanned values
 // k go to the new slab (in place), block and chunk aggregates to global.
@@ -696,57 +643,6 @@ __global__ void __launch_bounds__(kMaxWarps * kWarp) step_phase1(const StepParam
         }
     }
     block_err_flush(P, t, sm, eif, et);
-}
-
-// General path, phase 2: one thread per (column, subdomain): level 2 over all
-// blocks of the column, writes every block's carries.
-__global__ void step_phase2(const StepParams P) {
-    const int m = blockIdx.x * blockDim.x + threadIdx.x;
-    const int sub = blockIdx.z;
-    if (m >= P.nx) return;
-    const SubDev &S = P.subs[sub];
-    const int nblk = S.nblk;
-    auto B = [&](int c, int slot) {
-        return P.blkagg[((static_cast<size_t>(sub) * P.C + c) * 8 + slot) * P.nx + m];
-    };
-    const int n = S.n;
-    const int brow[4] = {0, 1, n - 2, n - 1};
-    // Same algebra as level2(), but every block's carries are produced.
-    auto Rc = [&](int c) { return min(P.R, n - c * P.R); };
-    double yb[4], xb[4], xt[4];
-    double Y = 0.0;
-    for (int c = 0; c < nblk; ++c) {
-        for (int q = 0; q < 4; ++q)
-            if (brow[q] / P.R == c) yb[q] = Y;
-        P.carry[((static_cast<size_t>(sub) * P.C + c) * 2 + 0) * P.nx + m] = Y;  // zero-chain Y0 (temp)
-        Y = fma(P.qp[Rc(c)], Y, B(c, 0));
-    }
-    double X = 0.0;
-    for (int c = nblk - 1; c >= 0; --c) {
-        for (int q = 0; q < 4; ++q)
-            if (brow[q] / P.R == c) xb[q] = X;
-        const double Y0c = P.carry[((static_cast<size_t>(sub) * P.C + c) * 2 + 0) * P.nx + m];
-        X = fma(P.qp[Rc(c)], X, fma(kapf(P.qp, P.s2, 0, Rc(c)), Y0c, B(c, 1)));
-    }
-    for (int q = 0; q < 4; ++q) {
-        const int c = brow[q] / P.R, l = brow[q] - c * P.R, R = Rc(c);
-        xt[q] = B(c, 2 + q) + kapf(P.qp, P.s2, l, R) * yb[q] + P.qp[R - l] * xb[q];
-    }
-    const double s0 = S.wt0 * xt[0] + S.wt1 * xt[1];
-    const double s1 = S.wb0 * xt[2] + S.wb1 * xt[3];
-    const double c0 = S.Mi00 * s0 + S.Mi01 * s1;
-    const double c1 = S.Mi10 * s0 + S.Mi11 * s1;
-    Y = -c0 / P.a;
-    for (int c = 0; c < nblk; ++c) {
-        P.carry[((static_cast<size_t>(sub) * P.C + c) * 2 + 0) * P.nx + m] = Y;
-        Y = fma(P.qp[Rc(c)], Y, B(c, 0));
-    }
-    X = -c1 / P.a;
-    for (int c = nblk - 1; c >= 0; --c) {
-        P.carry[((static_cast<size_t>(sub) * P.C + c) * 2 + 1) * P.nx + m] = X;
-        const double Yc = P.carry[((static_cast<size_t>(sub) * P.C + c) * 2 + 0) * P.nx + m];
-        X = fma(P.qp[Rc(c)], X, fma(kapf(P.qp, P.s2, 0, Rc(c)), Yc, B(c, 1)));
-    }
 }
 
 // General path, phase 2, warp per column: the same algebra as step_phase2, with the block recurrences

@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 const double *ut = P.UT + static_cast<size_t>(S.first + cr0) * P.nx + m;
 #pragma unroll
                 for (int l = 0; l < B; ++l)
-                    if (l < Lw) et = fmax(et, fabs(h[l] - ut[l * pitch]));
+                    if (l < Lw) et = nmax(et, fabs(h[l] - ut[l * pitch]));
             }
             // rows needed after the barrier (trace stencils, Robin-end interface rows)
             if (chunk_special) {
@@ -677,11 +677,11 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             if (blk == 0 && S.ltype == END_DIRI) {
                 const double g = sm.gin[lane];
                 if (S.iL_tr == -1) S.sendL[P.par_out][goff] = g;  // no overlap: the end node is the trace node
-                if (S.ifL >= 0) eif = fmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + step) * P.nx + m]));
+                if (S.ifL >= 0) eif = nmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + step) * P.nx + m]));
                 if (FEM) {  // the node's value enters the next step's transport and mass average
                     unew_slab[m] = g;
                 } else if (last) {
-                    et = fmax(et, fabs(g - P.UT[static_cast<size_t>(S.lo) * P.nx + m]));
+                    et = nmax(et, fabs(g - P.UT[static_cast<size_t>(S.lo) * P.nx + m]));
                     unew_slab[m] = g;
                 }
             } else if (blk == 0 && S.ltype == END_PHYS && last) {
@@ -690,11 +690,11 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             if (blk == nblk - 1 && S.rtype == END_DIRI) {
                 const double g = sm.gin[kWarp + lane];
                 if (S.iR_tr == n) S.sendR[P.par_out][goff] = g;
-                if (S.ifR >= 0) eif = fmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + step) * P.nx + m]));
+                if (S.ifR >= 0) eif = nmax(eif, fabs(g - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + step) * P.nx + m]));
                 if (FEM) {
                     unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + m] = g;
                 } else if (last) {
-                    et = fmax(et, fabs(g - P.UT[static_cast<size_t>(S.hi) * P.nx + m]));
+                    et = nmax(et, fabs(g - P.UT[static_cast<size_t>(S.hi) * P.nx + m]));
                     unew_slab[static_cast<size_t>(S.hi - S.lo) * P.nx + m] = g;
                 }
             } else if (blk == nblk - 1 && S.rtype == END_PHYS && last) {
@@ -726,9 +726,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                     S.sendR[P.par_out][goff] = g;
                 }
                 if (inblk(sp_row[4]))
-                    eif = fmax(eif, fabs(sm.xsp[4 * kWarp + lane] - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + step) * P.nx + m]));
+                    eif = nmax(eif, fabs(sm.xsp[4 * kWarp + lane] - P.Ulines[(static_cast<size_t>(S.ifL) * P.nt + step) * P.nx + m]));
                 if (inblk(sp_row[5]))
-                    eif = fmax(eif, fabs(sm.xsp[5 * kWarp + lane] - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + step) * P.nx + m]));
+                    eif = nmax(eif, fabs(sm.xsp[5 * kWarp + lane] - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + step) * P.nx + m]));
                 if (P.record)  // read back this block's recorded rows of u^{n+1} (stored above by this CTA)
                     for (int i = 0; i < FP.nrec; ++i) {
                         const int row = FP.rec_rows[i];
@@ -765,12 +765,12 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
         if (threadIdx.x == 0) {
             double a = 0.0, b = 0.0;
             for (int c = 0; c < NW; ++c) {
-                a = fmax(a, sm.red[c]);
-                b = fmax(b, sm.red[NW + c]);
+                a = nmax(a, sm.red[c]);
+                b = nmax(b, sm.red[NW + c]);
             }
             const size_t go = static_cast<size_t>(S.grp) * P.err_stride;  // replica of this CTA's subdomain
-            if (a > 0.0) atomic_max_pos(P.errIF + go, a);
-            if (b > 0.0 && P.errT) atomic_max_pos(P.errT + go, b);
+            if (err_pos(a)) atomic_max_pos(P.errIF + go, a);
+            if (err_pos(b) && P.errT) atomic_max_pos(P.errT + go, b);
         }
     }
     KFP_T(63)
@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(128) fem_finish(const StepParams P) {
             const double w = row[m], wn = row[(2 * j - P.nv >= 0) ? ml : mr];
             const double u = fma(fabs(fma(static_cast<double>(j), P.dnu, P.nu0)), wn - w, w);
             dst[static_cast<size_t>(r) * P.nx + m] = u;
-            if (P.UT) e = fmax(e, fabs(u - P.UT[static_cast<size_t>(j) * P.nx + m]));
+            if (P.UT) e = nmax(e, fabs(u - P.UT[static_cast<size_t>(j) * P.nx + m]));
         }
     }
     if (P.errT) {
@@ -807,8 +807,8 @@ __global__ void __launch_bounds__(128) fem_finish(const StepParams P) {
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
         __syncthreads();
         if (threadIdx.x == 0) {
-            e = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
-            if (e > 0.0) atomic_max_pos(P.errT + static_cast<size_t>(S.grp) * P.err_stride, e);
+            e = nmax(nmax(red[0], red[1]), nmax(red[2], red[3]));
+            if (err_pos(e)) atomic_max_pos(P.errT + static_cast<size_t>(S.grp) * P.err_stride, e);
         }
     }
 }
@@ -825,14 +825,14 @@ __global__ void __launch_bounds__(256) overlap_diff(const SubDev *subs, const in
     double e = 0.0;
     for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
          i += static_cast<size_t>(gridDim.x) * blockDim.x)
-        e = fmax(e, fabs(a[i] - b[i]));
+        e = nmax(e, fabs(a[i] - b[i]));
     __shared__ double red[8];
     e = warp_max(e);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < 8; ++w) e = fmax(e, red[w]);
-        if (e > 0.0) atomic_max_pos(errOV + static_cast<size_t>(L.grp) * err_stride, e);
+        for (int w = 1; w < 8; ++w) e = nmax(e, red[w]);
+        if (err_pos(e)) atomic_max_pos(errOV + static_cast<size_t>(L.grp) * err_stride, e);
     }
 }
 

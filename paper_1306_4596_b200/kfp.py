@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KFP_LIB_PATH") or os.path.join(_HERE, "libkfp.so")  # override: debugging builds only
 
-KFP_OK, KFP_E_INVAL, KFP_E_CFL, KFP_E_NOMEM, KFP_E_CUDA, KFP_E_STATE = 0, -1, -2, -3, -4, -6
+KFP_OK, KFP_E_INVAL, KFP_E_CFL, KFP_E_NOMEM, KFP_E_CUDA, KFP_E_STATE, KFP_E_NONFINITE = 0, -1, -2, -3, -4, -6, -7
 KIND = {"dirichlet": 0, "robin": 1}
 SCHEME = {"imex_fd": 0, "split_fem": 1}
 METRIC = {"err_T": 0, "err_if": 1, "overlap": 2}  # kfp_metric  # kfp_scheme (include/kfp.h)
@@ -235,10 +235,10 @@ class Problem:
               q: Optional[float] = None, out: Optional[np.ndarray] = None):
         """Setup + K iterations; returns the assembled u^K(T) (into `out`, e.g. a pinned buffer, if given)."""
         g = self.grid
-        if out is not None and not (out.dtype == np.float64 and out.flags.c_contiguous and out.size == (g.nv + 1) * g.nx):
-            raise ValueError("solve: out must be a C-contiguous float64 array of (nv+1)*nx elements")
-        else:
+        if out is None:
             out = np.empty((g.nv + 1, g.nx)) if copy else None
+        elif not (out.dtype == np.float64 and out.flags.c_contiguous and out.size == (g.nv + 1) * g.nx):
+            raise ValueError("solve: out must be a C-contiguous float64 array of (nv+1)*nx elements")
         if q is None:
             _check(load().kfp_swr_solve(self._h, KIND[kind], float(p), int(overlap), int(n_sub), int(K), _ptr(out)))
         else:

@@ -122,18 +122,6 @@ def test_fem_monodomain_tall_columns(kfp, nv, nx):
     assert np.array_equal(uT, UT)
 
 
-def test_fem_rejects_alternative_kernels(kfp, monkeypatch):
-    """The split-FEM scheme exists only in the per-step cluster kernel: KFP_WINDOW / KFP_COL requests are
-    ignored for it (the plan stays the FEM cluster kernel), never silently routed elsewhere."""
-    for env in ("KFP_WINDOW", "KFP_COL"):
-        monkeypatch.setenv(env, "1")
-        c = CASES["robin_S2"]
-        with kfp.Problem(ki.fem_problem(c.grid, c.seed)) as pb:
-            pb.setup(c.kind, c.p, c.ov, c.S, 2)
-            assert "fused-tma-cluster-fem" in pb.plan()
-        monkeypatch.delenv(env)
-
-
 def test_fem_batched_sweep_equals_individual(kfp):
     """The batched Robin-parameter sweep (Fig. 1's experiment) with the paper's scheme: every
     replica bitwise equals its individual solve."""

@@ -338,3 +338,69 @@ def test_gauss_seidel_converges_to_monodomain(orc):
     assert np.all(gs["err_if"][4:] <= ja["err_if"][4:] * (1 + 1e-12))
     gs = orc.swr(prob, "robin", 4.0, 0, 4, 160, schedule="gauss_seidel")
     assert gs["err_T"][-1] < 1e-11 * np.abs(gs["UT"]).max(), gs["err_T"][-1]
+
+
+def _check_scratch(gold, UT_max, err_exact, err_T, err_if):
+    assert abs(UT_max - gold["max_abs_UT"]) <= 1.5e-4 * gold["max_abs_UT"]
+    assert abs(err_exact - gold["err_exact_T"]) <= 1.5e-3 * gold["err_exact_T"]
+    for k, (eT, eI) in gold["history"].items():
+        k = int(k)
+        assert abs(err_T[k - 1] - eT) <= 1.5e-4 * eT, (k, err_T[k - 1], eT)
+        assert abs(err_if[k - 1] - eI) <= 1.5e-4 * eI, (k, err_if[k - 1], eI)
+
+
+def _gold(name):
+    with open(os.path.join(GOLDEN, f"survey_scratch_{name}.json")) as fh:
+        return json.load(fh)
+
+
+def test_subdomain_ranges_match_survey(orc):
+    """Overlap placement (R9; O2 of SURVEY.md §8(c)) against the survey's explicit node ranges:
+    c1 [0,132] / [124,256]; c3 [2048 s, 2048 (s+1)]; c4 [1024 s - 2, 1024 (s+1) + 2] clipped to
+    [0, 32768] -- and, for an odd overlap (where floor and ceil differ), R9's text: the left
+    subdomain extends to c + ceil(ov/2), the right one starts at c - floor(ov/2).  The mode-reduced
+    oracle's own decomposition must agree."""
+    from oracle.modal import _subdomains
+
+    gold = _gold("c1")["node_ranges"]
+    cases = [((256, 2, 8), (gold["lo"], gold["hi"])),
+             ((16384, 8, 0), ([2048 * s for s in range(8)], [2048 * (s + 1) for s in range(8)])),
+             ((32768, 32, 4), ([max(0, 1024 * s - 2) for s in range(32)],
+                               [min(32768, 1024 * (s + 1) + 2) for s in range(32)])),
+             ((64, 2, 3), ([0, 31], [34, 64])),
+             ((60, 3, 5), ([0, 18, 38], [23, 43, 60]))]
+    for (nv, S, ov), (lo, hi) in cases:
+        olo, ohi = orc.subdomains(nv, S, ov)
+        assert list(olo) == list(lo) and list(ohi) == list(hi), (nv, S, ov, olo, ohi)
+        mlo, mhi = _subdomains(nv, S, ov)
+        assert mlo == list(lo) and mhi == list(hi)
+
+
+def test_survey_scratch_histories_c1(orc):
+    """c1 (Dirichlet, overlap 8: exercises R9's placement and err_if at Dirichlet interface ends) on the
+    C oracle at full size, against the survey's independent scratch model
+    (tests/golden/survey_scratch_c1.json)."""
+    run = ki.config("c1")
+    r = orc.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, 10)
+    lo, hi = r["lo"], r["hi"]
+    assert list(lo) == [0, 124] and list(hi) == [132, 256]
+    g = run.grid
+    x = np.arange(g.nx) / g.nx
+    v = -g.vmax + np.arange(g.nv + 1) * (2 * g.vmax / g.nv)
+    u_ex = math.exp(-g.t_final) * np.outer(g.vmax ** 2 - v ** 2, np.sin(2 * np.pi * x))
+    _check_scratch(_gold("c1"), np.abs(r["UT"]).max(), np.abs(r["UT"] - u_ex).max(), r["err_T"], r["err_if"])
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_survey_scratch_histories_modal(name):
+    """c2 (S = 2 Robin p = 4) and c3 (S = 8 Robin p = 8, K = 15) at full size on the mode-reduced oracle
+    (exact for the manufactured data, pinned to the 2-D oracle by test_mode_reduced_oracle_agrees_with_direct),
+    against the survey's independent scratch histories (tests/golden/survey_scratch_{c2,c3}.json)."""
+    from oracle.modal import max_abs_real
+
+    run = ki.config(name)
+    g = run.grid
+    m = modal_swr(g, run.kind, run.p, run.overlap, run.n_sub, run.K)
+    v = -g.vmax + np.arange(g.nv + 1) * (2 * g.vmax / g.nv)
+    c_ex = math.exp(-g.t_final) * (g.vmax ** 2 - v ** 2)
+    _check_scratch(_gold(name), max_abs_real(m["C"], g.nx), max_abs_real(m["C"] - c_ex, g.nx), m["err_T"], m["err_if"])
