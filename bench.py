@@ -232,7 +232,7 @@ def bench_single(args):
 
     # end to end through the public API with host buffers (create -> solve -> read back): the input tables and
     # the result live in pinned host memory (allocated outside the timed region)
-    e2e_steps = max(1, min(args.steps, 2))
+    e2e_steps = 0 if args.no_e2e else max(1, min(args.steps, 2))
 
     def pinned_copy(a):
         t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
@@ -254,8 +254,8 @@ def bench_single(args):
             d2h = uT.nbytes + h[0].nbytes + h[1].nbytes
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    e2e_value = updates / (e2e_ms / 1e3)
+    e2e_ms = e0.elapsed_time(e1) / max(1, e2e_steps)
+    e2e_value = updates / (e2e_ms / 1e3) if e2e_steps else None
 
     cpu = None
     if not args.no_cpu:
@@ -309,6 +309,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (kernel experiments)")
     args = ap.parse_args()
     if args.impl == "reference":
         return bench_reference(args)

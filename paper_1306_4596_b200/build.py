@@ -5,6 +5,7 @@ kernel perturbed by 1e-3, kfp_api.cu base_params); tests/test_gpu_parity.py chec
 fails on it (the suite is sensitive to a plausible kernel mistake).  Never loaded by the product path."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -12,8 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "kfp_api.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "kfp_fused.cuh"), os.path.join(HERE, "csrc", "kfp_device.cuh"),
-              os.path.join(ROOT, "include", "kfp.h")]
+DEPS = SRC + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "kfp.h")]
 LIB = os.path.join(HERE, "libkfp.so")
 MUTANT = os.path.join(HERE, "libkfp_mut.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
