@@ -122,8 +122,21 @@ def oracle_sample(run: ki.Run, budget_updates: float = 2.5e9):
     return ki.scaled(run, nt=nt, K=1, t_final=dt * nt, name=run.name + "_sample")
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def run_cpu_oracle(run: ki.Run, steps: int = 1):
-    """Time the oracle as it stands on the host cores; returns (updates/s, cores, sample text)."""
+    """Time the oracle as it stands on the host cores; returns (updates/s, cores, sample text, s per step)."""
     import oracle
 
     sample = oracle_sample(run)
@@ -135,7 +148,8 @@ def run_cpu_oracle(run: ki.Run, steps: int = 1):
         oracle.swr(prob, sample.kind, sample.p, sample.overlap, sample.n_sub, sample.K, q=sample.q)
     dt = time.perf_counter() - t0
     text = (f"{run.name} grid {g.nx}x{g.nv}, same dt/CFL, window cut to n_t={g.nt} steps, K=1, "
-            f"plus the monodomain window; {updates:.3g} updates per step")
+            f"plus the monodomain window; {updates:.3g} updates per step; host: {cpu_model()}, "
+            f"nproc={os.cpu_count()}, OpenMP threads={oracle.num_threads()}")
     return updates * steps / dt, oracle.num_threads(), text, dt / steps
 
 
@@ -152,7 +166,8 @@ def bench_reference(args):
         "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "config": {"workload": run.name, "oracle_sample": text},
-        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "oracle", "sample": text},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "oracle", "sample": text,
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -182,11 +197,9 @@ def bench_single(args):
         pb.reset()
         pb.iterate(run.K)
 
-    # W untimed warm-up solves, continued (untimed) until >= 5 s of warm-up: a box that just came up has
-    # been seen to run the first seconds ~10 % slow at full clocks; the line reports the count actually run
-    t_w = time.perf_counter()
+    # exactly W untimed warm-up solves
     warm = 0
-    while warm < args.warmup or (time.perf_counter() - t_w < 5.0 and warm < args.warmup + 200):
+    while warm < args.warmup:
         one()
         torch.cuda.synchronize()
         warm += 1
@@ -199,6 +212,7 @@ def bench_single(args):
     clocks.start()
     step_kernel_ms = 0.0
     ms = 0.0
+    step_ms = []
     torch.cuda.synchronize()
     for _ in range(args.steps):
         if flush is not None:
@@ -211,7 +225,8 @@ def bench_single(args):
         _, kms = pb.last_timing()
         step_kernel_ms += kms
         torch.cuda.synchronize()
-        ms += ev0.elapsed_time(ev1)
+        step_ms.append(ev0.elapsed_time(ev1))
+        ms += step_ms[-1]
     clk = clocks.stop()
     launches = pb.launch_count() - launches0
     updates = run.updates
@@ -257,10 +272,50 @@ def bench_single(args):
     e2e_ms = e0.elapsed_time(e1) / max(1, e2e_steps)
     e2e_value = updates / (e2e_ms / 1e3) if e2e_steps else None
 
+    # where an end-to-end solve spends its time (separate, untimed for the headline: a host synchronisation
+    # after each public call): create (table H2D), setup (allocations, the monodomain reference with its
+    # recorded interface lines, constant tables), the K iterations, the D2H of u(T) and the history, destroy
+    phases = None
+    mono = None
+    if e2e_steps:
+        ph = {}
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        q = Problem(prob_pinned, device=dev)
+        q.set_stream(stream.cuda_stream)
+        torch.cuda.synchronize()
+        ph["create"], t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+        q.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
+        torch.cuda.synchronize()
+        ph["setup_incl_monodomain"], t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+        q.iterate(run.K)
+        torch.cuda.synchronize()
+        ph["iterate"], t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+        for s_ in range(run.n_sub):
+            q.subdomain_uT(s_)
+        q.history()
+        ph["d2h"], t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+        q.close()
+        torch.cuda.synchronize()
+        ph["destroy"] = (time.perf_counter() - t) * 1e3
+        phases = {k: round(v, 3) for k, v in ph.items()}
+        # the monodomain reference alone (reported separately, N_x N_v N_t updates / s)
+        with Problem(prob, device=dev) as q:
+            q.set_stream(stream.cuda_stream)
+            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            m0.record(stream)
+            q.monodomain(copy=False)
+            m1.record(stream)
+            torch.cuda.synchronize()
+            mms = m0.elapsed_time(m1)
+            mono = {"value": g.nx * g.nv * g.nt / (mms / 1e3), "unit": "updates/s", "ms": mms}
+
     cpu = None
     if not args.no_cpu:
         v, cores, text, _ = run_cpu_oracle(run, 1)
-        cpu = {"value": v, "unit": "updates/s", "cores": cores, "kind": "oracle", "sample": text}
+        cpu = {"value": v, "unit": "updates/s", "cores": cores, "kind": "oracle", "sample": text,
+               "cpu_model": cpu_model(), "nproc": os.cpu_count()}
 
     line = {
         "metric": "grid-point updates/s (N_x*N_v*N_t*K / wall)", "value": value, "unit": "updates/s",
@@ -279,7 +334,9 @@ def bench_single(args):
                      "traffic_source": "profiles/*_ncu_summary.json (ncu --set full, same plan)" if traffic else None,
                      "bytes_per_launch": bytes_per_launch, "avg_launch_us": per_launch_s * 1e6},
         "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": pb.h2d_bytes,
-                "d2h_bytes_per_step": int(d2h)},
+                "d2h_bytes_per_step": int(d2h), "ms": e2e_ms, "phases_ms": phases},
+        "monodomain": mono,
+        "ms_per_step_median": float(np.median(step_ms)), "ms_per_step_all": [round(x, 3) for x in step_ms],
         "gpu_launches": int(launches),
         "clocks": clk,
         "cpu_baseline": cpu,
@@ -300,19 +357,39 @@ def _json_stdout():
     return out
 
 
+def spawn_ranks(args):
+    """`bench.py --gpus N` without torchrun: launch N ranks (one per GPU, NCCL) through torch.distributed.run
+    on 127.0.0.1 and pass rank 0's JSON line through (the driver's own launch is the same command)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, text=True)
+    for line in r.stdout.splitlines():
+        if line.startswith("{"):
+            print(line, flush=True)
+    return r.returncode
+
+
 def main():
     _json_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (kernel experiments)")
+    ap.add_argument("--chunks", type=int, default=4, help="N > 1: time chunks of the overlapped trace exchange")
     args = ap.parse_args()
     if args.impl == "reference":
         return bench_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
         from paper_1306_4596_b200 import dist

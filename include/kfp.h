@@ -172,6 +172,22 @@ kfp_status kfp_swr_set_initial_trace(kfp_problem pb, int32_t i, int32_t dir, con
  * problem's stream.  KFP_E_STATE if more than K_max iterations in total. */
 kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter);
 
+/* Time-chunked Jacobi iteration for overlapping the cross-GPU trace exchange with compute (step n
+ * of iteration k+1 needs only trace row n of iteration k; SURVEY §8(e) "Overlap").  The window's nt steps
+ * are split into nchunks chunks, chunk c = steps [c*nt/nchunks, (c+1)*nt/nchunks) = trace rows of the same
+ * indices.  kfp_swr_iterate_chunk launches chunk `chunk` of the current iteration on the problem's stream
+ * (chunks in order 0..nchunks-1; the last one completes the iteration, like kfp_swr_iterate(pb, 1)); before
+ * its first step the stream waits for the event most recently recorded by kfp_swr_chunk_recv_done(chunk)
+ * (the previous iteration's incoming edge rows of the chunk), after its last step the library records that
+ * the chunk's outgoing edge rows are written.  kfp_swr_chunk_send_wait makes `stream` (a cudaStream_t, e.g.
+ * the communication stream) wait for that; kfp_swr_chunk_recv_done records on `stream` that the incoming
+ * rows of the chunk have arrived.  Unpipelined Jacobi only (else KFP_E_STATE); KFP_E_INVAL for a bad chunk;
+ * KFP_E_STATE for chunks out of order or a changed nchunks inside an iteration.  kfp_swr_reset waits for the
+ * last recorded arrivals before it zeroes the incoming traces. */
+kfp_status kfp_swr_iterate_chunk(kfp_problem pb, int32_t chunk, int32_t nchunks);
+kfp_status kfp_swr_chunk_send_wait(kfp_problem pb, void *stream, int32_t chunk);
+kfp_status kfp_swr_chunk_recv_done(kfp_problem pb, void *stream, int32_t chunk);
+
 /* Device pointers of the cross-block exchange buffers, each [nt][nx] fp64
  * (row n-1 = value at t_n), for the parity iteration `k & 1` that the NEXT
  * kfp_swr_iterate call reads: after iteration k the caller must copy the left

@@ -253,6 +253,11 @@ struct kfp_problem_s {
     std::vector<double *> zero_on_reset;  // parity-0 incoming buffers
 
     int64_t launches = 0;
+    // time-chunked iterations (kfp_swr_iterate_chunk): per chunk, "outgoing rows written" and "incoming rows
+    // arrived" events; the next chunk expected
+    int nchunks = 0, chunk_next = 0;
+    std::vector<cudaEvent_t> chunk_sent, chunk_recv;
+    std::vector<char> chunk_recv_set;
     std::vector<cudaEvent_t> ev;  // 2 per iteration of the last iterate call + 2 around it
     int ev_used = 0;
     std::string plan_text;
@@ -926,6 +931,8 @@ void kfp_problem_destroy(kfp_problem pb) {
     free_swr(pb);
     for (void *p : pb->allocs) cudaFree(p);
     for (cudaEvent_t e : pb->ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : pb->chunk_sent) cudaEventDestroy(e);
+    for (cudaEvent_t e : pb->chunk_recv) cudaEventDestroy(e);
     if (pb->own_stream) cudaStreamDestroy(pb->own_stream);
     delete pb;
 }
@@ -1270,6 +1277,11 @@ kfp_status kfp_swr_reset(kfp_problem pb) {
         return KFP_E_STATE;
     }
     KFP_CUDA(cudaSetDevice(pb->device));
+    // chunked exchange of an earlier solve: the traces it received must have landed before they are zeroed
+    for (int c = 0; c < pb->nchunks; ++c)
+        if (pb->chunk_recv_set[c]) KFP_CUDA(cudaStreamWaitEvent(pb->stream, pb->chunk_recv[c], 0));
+    std::fill(pb->chunk_recv_set.begin(), pb->chunk_recv_set.end(), 0);
+    pb->chunk_next = 0;
     const size_t TR = (size_t)pb->nt * pb->nx;
     for (double *p : pb->zero_on_reset) KFP_CUDA(cudaMemsetAsync(p, 0, TR * sizeof(double), pb->stream));
     if (pb->edge_recvL[0]) KFP_CUDA(cudaMemsetAsync(pb->edge_recvL[0], 0, TR * sizeof(double), pb->stream));
@@ -1453,6 +1465,108 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
         pb->k_done = k;
     }
     KFP_CUDA(cudaEventRecord(pb->ev[1], pb->stream));
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_iterate_chunk(kfp_problem pb, int32_t chunk, int32_t nchunks) {
+    if (!pb || !pb->setup) {
+        set_err("kfp_swr_iterate_chunk: no setup");
+        return KFP_E_STATE;
+    }
+    if (nchunks < 1 || nchunks > pb->nt || chunk < 0 || chunk >= nchunks) {
+        set_err("kfp_swr_iterate_chunk: chunk %d of %d (need 0 <= chunk < nchunks <= nt=%d)", chunk, nchunks, pb->nt);
+        return KFP_E_INVAL;
+    }
+    if (pb->pipe > 1 || pb->gauss_seidel) {
+        set_err("kfp_swr_iterate_chunk: needs the unpipelined Jacobi schedule");
+        return KFP_E_STATE;
+    }
+    KFP_CUDA(cudaSetDevice(pb->device));
+    if (nchunks != pb->nchunks) {  // (re)create the chunk events
+        if (pb->chunk_next != 0) {
+            set_err("kfp_swr_iterate_chunk: the iteration in progress has %d chunks", pb->nchunks);
+            return KFP_E_STATE;
+        }
+        for (cudaEvent_t e : pb->chunk_sent) cudaEventDestroy(e);
+        for (cudaEvent_t e : pb->chunk_recv) cudaEventDestroy(e);
+        pb->chunk_sent.assign(nchunks, nullptr);
+        pb->chunk_recv.assign(nchunks, nullptr);
+        pb->chunk_recv_set.assign(nchunks, 0);
+        for (int c = 0; c < nchunks; ++c) {
+            KFP_CUDA(cudaEventCreateWithFlags(&pb->chunk_sent[c], cudaEventDisableTiming));
+            KFP_CUDA(cudaEventCreateWithFlags(&pb->chunk_recv[c], cudaEventDisableTiming));
+        }
+        pb->nchunks = nchunks;
+    }
+    if (chunk != pb->chunk_next) {
+        set_err("kfp_swr_iterate_chunk: expected chunk %d, got %d", pb->chunk_next, chunk);
+        return KFP_E_STATE;
+    }
+    if (chunk == 0 && pb->k_done + 1 > pb->K_max) {
+        set_err("kfp_swr_iterate_chunk: %d iterations exceed K_max=%d", pb->k_done + 1, pb->K_max);
+        return KFP_E_STATE;
+    }
+    const int k = pb->k_done + 1;
+    StepParams P = base_params(pb);
+    P.subs = pb->d_subs;
+    P.send_robin = (pb->kind == KFP_ROBIN);
+    P.p = pb->p;
+    P.UT = pb->d_UT;
+    P.Ulines = pb->d_Ulines;
+    P.blkagg = pb->d_blkagg;
+    P.chkagg = pb->d_chkagg;
+    P.carry = pb->d_carry;
+    P.ovrec = pb->ovrec ? 1 : 0;
+    P.par_in = P.par_in_lo = (k - 1) & 1;
+    P.par_out = k & 1;
+    P.errT = pb->d_errT + (k - 1);
+    P.errIF = pb->d_errIF + (k - 1);
+    P.err_stride = pb->K_max;
+    // the incoming edge rows of this chunk (the previous iteration's) must have arrived
+    if (pb->chunk_recv_set[chunk]) KFP_CUDA(cudaStreamWaitEvent(pb->stream, pb->chunk_recv[chunk], 0));
+    const int nloc = (int)pb->subs.size();
+    const int n0 = (int)((int64_t)chunk * pb->nt / nchunks), n1 = (int)((int64_t)(chunk + 1) * pb->nt / nchunks);
+    for (int n = n0; n < n1; ++n) {
+        P.last = (n + 1 == pb->nt);
+        if (kfp_status st = launch_step(pb, pb->plan, P, nloc, n, pb->fd)) return st;
+    }
+    KFP_CUDA(cudaEventRecord(pb->chunk_sent[chunk], pb->stream));  // outgoing rows [n0, n1) written
+    if (chunk + 1 == nchunks) {
+        if (pb->scheme == KFP_SCHEME_SPLIT_FEM) {
+            int rows = 0;
+            for (const SubDev &sd : pb->subs) rows = std::max(rows, sd.hi - sd.lo + 1);
+            if (kfp_status st = launch_fem_finish(pb, P, nloc, rows)) return st;
+        }
+        if (pb->ovrec && pb->npairs > 0) {
+            kfp::overlap_diff<<<dim3(64, 1, pb->npairs), 256, 0, pb->stream>>>(pb->d_subs, pb->d_pairs, pb->nt, pb->nx,
+                                                                             pb->d_errOV + (k - 1), pb->K_max);
+            pb->launches += 1;
+            KFP_CUDA(cudaGetLastError());
+        }
+        pb->k_done = k;
+        pb->chunk_next = 0;
+    } else {
+        pb->chunk_next = chunk + 1;
+    }
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_chunk_send_wait(kfp_problem pb, void *stream, int32_t chunk) {
+    if (!pb || !pb->setup || chunk < 0 || chunk >= pb->nchunks) {
+        set_err("kfp_swr_chunk_send_wait: no chunked iteration or bad chunk %d", chunk);
+        return KFP_E_INVAL;
+    }
+    KFP_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pb->chunk_sent[chunk], 0));
+    return KFP_OK;
+}
+
+kfp_status kfp_swr_chunk_recv_done(kfp_problem pb, void *stream, int32_t chunk) {
+    if (!pb || !pb->setup || chunk < 0 || chunk >= pb->nchunks) {
+        set_err("kfp_swr_chunk_recv_done: no chunked iteration or bad chunk %d", chunk);
+        return KFP_E_INVAL;
+    }
+    KFP_CUDA(cudaEventRecord(pb->chunk_recv[chunk], static_cast<cudaStream_t>(stream)));
+    pb->chunk_recv_set[chunk] = 1;
     return KFP_OK;
 }
 

@@ -3,10 +3,16 @@
 Rank r of a world of g solves subdomains [r*S/g, (r+1)*S/g).
 Within an iteration the subdomains are independent (the parallel schedule of
 the Remark at PAPER.md:594-597); the only data-path exchange is the
-whole-window interface traces of the two block edges, sent to the neighbour
-ranks after every iteration with NCCL point-to-point send/recv
-(torch.distributed, NVLink/NVSwitch on one box), and the per-iteration error
-history reduced with one all_reduce(MAX) at the end.
+interface traces of the two block edges, sent to the neighbour ranks with NCCL
+point-to-point send/recv (torch.distributed, NVLink/NVSwitch on one box), and
+the per-iteration error history reduced with one all_reduce(MAX) at the end.
+
+Overlap (``chunks > 1``): step n of iteration k+1 needs only trace row n of
+iteration k, so the window is cut into time chunks; chunk c's edge
+rows go out on a communication stream as soon as the library has written them
+(kfp_swr_chunk_send_wait), and chunk c of the next iteration waits only for
+chunk c's incoming rows (kfp_swr_chunk_recv_done).  The exchange of the last
+chunk overlaps the next iteration's first chunks; the host never waits.
 
 The local solver is pluggable so that this host logic is testable on CPU:
 ``CudaBlock`` wraps the C-ABI (``kfp_swr_bind_edge_buffers`` points the
@@ -47,6 +53,7 @@ class CudaBlock:
         # after the current stream) and the timing events all sit on it (the legacy default stream, handle 0,
         # would leave the library on its own non-blocking stream, unordered with the exchange)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=device)
+        self.comm = torch.cuda.Stream(device=device)  # the chunked exchange (NCCL orders itself after it)
         torch.cuda.set_stream(self.stream)
         self.pb = Problem(prob, device=device)
         self.pb.set_stream(self.stream.cuda_stream)
@@ -68,6 +75,20 @@ class CudaBlock:
 
     def iterate(self):
         self.pb.iterate(1)
+
+    def iterate_chunk(self, c: int, nchunks: int):
+        self.pb.iterate_chunk(c, nchunks)
+
+    def comm_begin(self, c: int):
+        """Enter the communication stream once chunk c's outgoing rows are written (returns a context)."""
+        ctx = torch.cuda.stream(self.comm)
+        ctx.__enter__()
+        self.pb.chunk_send_wait(self.comm.cuda_stream, c)
+        return ctx
+
+    def comm_end(self, c: int, ctx):
+        self.pb.chunk_recv_done(self.comm.cuda_stream, c)
+        ctx.__exit__(None, None, None)
 
     def history(self):
         eT, eI = self.pb.history()
@@ -94,14 +115,37 @@ def exchange(block, rank: int, world: int, parity: int):
             req.wait()
 
 
-def run_swr(block, K: int, rank: int, world: int, on_iterate=None):
-    """K Jacobi iterations with the edge exchange after each; returns the global (err_T, err_if).
-    on_iterate(block) runs after each iteration's launches (e.g. to read the library's window timing)."""
+def exchange_chunk(block, rank: int, world: int, parity: int, c: int, nchunks: int, nt: int):
+    """Send rows [c nt / C, (c+1) nt / C) of this block's outgoing edge traces of `parity` to the neighbour
+    ranks and receive theirs (on the block's communication stream when it has one; the requests make that
+    stream, not the host, wait)."""
+    n0, n1 = c * nt // nchunks, (c + 1) * nt // nchunks
+    ctx = block.comm_begin(c) if hasattr(block, "comm_begin") else None
+    ops = []
+    if block.has_left:
+        ops.append(dist.P2POp(dist.isend, block.send_left[parity][n0:n1], rank - 1))
+        ops.append(dist.P2POp(dist.irecv, block.recv_left[parity][n0:n1], rank - 1))
+    if block.has_right:
+        ops.append(dist.P2POp(dist.isend, block.send_right[parity][n0:n1], rank + 1))
+        ops.append(dist.P2POp(dist.irecv, block.recv_right[parity][n0:n1], rank + 1))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    if ctx is not None:
+        block.comm_end(c, ctx)
+
+
+def run_swr(block, K: int, rank: int, world: int, chunks: int = 1, nt: int = 0):
+    """K Jacobi iterations; returns the global (err_T, err_if).  chunks == 1: whole-window exchange after each
+    iteration.  chunks > 1: the time-chunked protocol (module docstring); nt = steps per window."""
     for k in range(1, K + 1):
-        block.iterate()  # reads recv_*[(k-1)&1], writes send_*[k&1]
-        if on_iterate:
-            on_iterate(block)
-        exchange(block, rank, world, k & 1)
+        if chunks <= 1:
+            block.iterate()  # reads recv_*[(k-1)&1], writes send_*[k&1]
+            exchange(block, rank, world, k & 1)
+        else:
+            for c in range(chunks):
+                block.iterate_chunk(c, chunks)  # waits (on the device) for chunk c of recv_*[(k-1)&1]
+                exchange_chunk(block, rank, world, k & 1, c, chunks, nt)
     eT, eI = block.history()
     hist = torch.stack([eT, eI])
     if world > 1:
@@ -139,28 +183,16 @@ def bench_main(args, default_workload, clock_sampler=None, peaks=None):
     blk = CudaBlock(prob, run.kind, run.p, run.overlap, run.n_sub, run.K, rank, world, local)
     stream = blk.stream  # current (CudaBlock made it so)
 
-    kernel_ms = [0.0]
+    chunks = max(1, min(int(getattr(args, "chunks", 4) or 1), g.nt))
 
-    def tally(b):  # the step launches of the iteration just run (library events on the same stream)
-        kernel_ms[0] += b.pb.last_timing()[1]
-
-    def one(b, timed=False):
+    def one(b):
         b.reset()
-        return run_swr(b, run.K, rank, world, tally if timed else None)
+        return run_swr(b, run.K, rank, world, chunks=chunks, nt=g.nt)
 
-    # W untimed warm-up solves, then more until >= 5 s of warm-up (as bench.py); every rank runs the same
-    # count (the ranks exchange traces), agreed by a MAX all-reduce
-    t_w = time.perf_counter()
+    # exactly W untimed warm-up solves
     for _ in range(args.warmup):
         one(blk)
-    torch.cuda.synchronize()
-    per = (time.perf_counter() - t_w) / max(1, args.warmup)
-    extra = torch.tensor([min(200, max(0, int((5.0 - (time.perf_counter() - t_w)) / max(per, 1e-3)) + 1))],
-                         device=dev, dtype=torch.int64)
-    dist.all_reduce(extra, op=dist.ReduceOp.MAX)
-    for _ in range(int(extra.item())):
-        one(blk)
-    warm = args.warmup + int(extra.item())
+    warm = args.warmup
     dist.barrier()
     torch.cuda.synchronize()
     clocks = clock_sampler(local) if clock_sampler else None
@@ -169,8 +201,12 @@ def bench_main(args, default_workload, clock_sampler=None, peaks=None):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = blk.pb.launch_count()
     e0.record(stream)
-    for _ in range(args.steps):
-        one(blk, timed=True)
+    step_ev = []
+    for _ in range(args.steps):  # no host synchronisation inside the timed region
+        one(blk)
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        step_ev.append(ev)
     e1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop() if clocks else None
@@ -184,8 +220,17 @@ def bench_main(args, default_workload, clock_sampler=None, peaks=None):
     ends = 2 * (blk.s_end - blk.s_begin)  # end nodes that are not unknowns (Dirichlet / physical); Robin: upper bound
     bytes_per_launch = 16.0 * g.nx * (rows - ends)
     step_launches = g.nt * run.K * args.steps
-    per_launch = torch.tensor([kernel_ms[0] / 1e3 / step_launches], device=dev)
+    # average step-launch time: the timed region over its step launches (an upper bound: the region also
+    # holds the exchange waits and the error reductions; conservative for the roofline fraction)
+    per_launch = torch.tensor([float(ms.item()) / 1e3 / step_launches], device=dev)
     dist.all_reduce(per_launch, op=dist.ReduceOp.MAX)
+    sms = []
+    prev = e0
+    for ev in step_ev:
+        sms.append(prev.elapsed_time(ev))
+        prev = ev
+    med = torch.tensor([float(np.median(sms))], device=dev)
+    dist.all_reduce(med, op=dist.ReduceOp.MAX)
     plan = blk.pb.plan()
     ranges = [blk.pb.subdomain_range(s) for s in range(blk.s_begin, blk.s_end)]  # for the e2e output buffers
     blk.close()
@@ -222,10 +267,12 @@ def bench_main(args, default_workload, clock_sampler=None, peaks=None):
         line = {
             "metric": "grid-point updates/s (N_x*N_v*N_t*K / wall)", "value": value, "unit": "updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": warm, "ms_per_step": ms / args.steps,
+            "ms_per_step_median": float(med.item()),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": run.name, "nx": g.nx, "nv": g.nv, "nt": g.nt, "K": run.K, "n_sub": run.n_sub,
                        "kind": run.kind, "overlap": run.overlap, "plan": plan,
-                       "parallelism": f"v-subdomain blocks x{world}, NCCL P2P",
+                       "parallelism": f"v-subdomain blocks x{world}, NCCL P2P in {chunks} time chunks "
+                                      "overlapped with compute",
                        "l2": "inputs larger than L2", "updates_per_step": run.updates},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": None, "peak_kind": peak_kind,

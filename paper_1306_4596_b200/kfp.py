@@ -28,6 +28,7 @@ SYMBOLS = (
     "kfp_swr_subdomain_uT", "kfp_swr_subdomain_range", "kfp_swr_trace", "kfp_monodomain_uT", "kfp_launch_count",
     "kfp_plan", "kfp_last_timing", "kfp_last_error",
     "kfp_swr_set_overlap_error", "kfp_swr_overlap_history", "kfp_swr_iterate_until", "kfp_swr_set_pipeline",
+    "kfp_swr_iterate_chunk", "kfp_swr_chunk_send_wait", "kfp_swr_chunk_recv_done",
 )
 
 
@@ -96,6 +97,9 @@ def load(path: str = LIB_PATH):
         "kfp_swr_set_pipeline": (i32, [vp, i32]),
         "kfp_swr_overlap_history": (i32, [vp, i32, i32, ctypes.POINTER(i32), vp]),
         "kfp_swr_iterate_until": (i32, [vp, i32, dbl, i32, ctypes.POINTER(i32)]),
+        "kfp_swr_iterate_chunk": (i32, [vp, i32, i32]),
+        "kfp_swr_chunk_send_wait": (i32, [vp, vp, i32]),
+        "kfp_swr_chunk_recv_done": (i32, [vp, vp, i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -218,6 +222,16 @@ class Problem:
 
     def iterate(self, n: int = 1):
         _check(load().kfp_swr_iterate(self._h, int(n)))
+
+    def iterate_chunk(self, chunk: int, nchunks: int):
+        """Launch chunk `chunk` of the current iteration (time-chunked exchange, include/kfp.h)."""
+        _check(load().kfp_swr_iterate_chunk(self._h, int(chunk), int(nchunks)))
+
+    def chunk_send_wait(self, stream_handle: int, chunk: int):
+        _check(load().kfp_swr_chunk_send_wait(self._h, ctypes.c_void_p(stream_handle), int(chunk)))
+
+    def chunk_recv_done(self, stream_handle: int, chunk: int):
+        _check(load().kfp_swr_chunk_recv_done(self._h, ctypes.c_void_p(stream_handle), int(chunk)))
 
     def edge_buffers(self, parity: int):
         """(send_left, recv_left, send_right, recv_right) device pointers (int or None)."""

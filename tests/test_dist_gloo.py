@@ -99,6 +99,13 @@ class OracleBlock:
         self.eT.append(eT)
         self.eI.append(eI)
 
+    def iterate_chunk(self, c, nchunks):
+        """The time-chunked protocol (dist.exchange_chunk): the oracle solves the whole window with the first
+        chunk (every incoming row of the previous iteration has arrived by then); the exchange still moves
+        one chunk of rows at a time."""
+        if c == 0:
+            self.iterate()
+
     def history(self):
         return torch.tensor(self.eT, dtype=torch.float64), torch.tensor(self.eI, dtype=torch.float64)
 
@@ -109,14 +116,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, out):
+def _worker(rank, world, port, name, out, chunks=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1306_4596_b200.dist import run_swr
 
     run = RUNS[name]
     blk = OracleBlock(ki.make_problem(run), run, rank, world)
-    eT, eI = run_swr(blk, run.K, rank, world)
+    eT, eI = run_swr(blk, run.K, rank, world, chunks=chunks, nt=run.grid.nt)
     out[rank] = (eT, eI, {s: blk.uT[s] for s in blk.uT})
     dist.barrier()
     dist.destroy_process_group()
@@ -136,6 +143,27 @@ def test_two_rank_gloo_matches_single_process(orc, name):
             assert np.array_equal(a, ref["uT_sub"][s]), (rank, s)
     # both ranks together hold every subdomain
     assert sorted(list(out[0][2]) + list(out[1][2])) == list(range(run.n_sub))
+
+
+@pytest.mark.parametrize("name,world,chunks", [("robin4", 2, 4), ("dirichlet4", 2, 4), ("fem_robin_pq4", 2, 3),
+                                               ("robin_pq4", 4, 1), ("dirichlet4", 4, 3)])
+def test_chunked_exchange_matches_single_process(orc, name, world, chunks):
+    """The overlapped, time-chunked exchange protocol (dist.exchange_chunk; chunks of 30 // C rows, a ragged
+    last chunk for C = 4) and world size 4 (one subdomain per rank: both edges cross ranks): bitwise the
+    single-process oracle, like the whole-window exchange."""
+    run = RUNS[name]
+    ref = orc.swr(ki.make_problem(run), run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), name, out, chunks), nprocs=world, join=True)
+    held = []
+    for rank in range(world):
+        eT, eI, slabs = out[rank]
+        assert np.array_equal(eT, ref["err_T"]) and np.array_equal(eI, ref["err_if"])
+        for s, a in slabs.items():
+            assert np.array_equal(a, ref["uT_sub"][s]), (rank, s)
+        held += list(slabs)
+    assert sorted(held) == list(range(run.n_sub))
 
 
 def test_block_partition():

@@ -159,6 +159,59 @@ def test_block_split_matches_single_process(kfp):
     B.close()
 
 
+@pytest.mark.parametrize("nchunks", [1, 4, 7])
+def test_block_split_chunked_exchange(kfp, nchunks):
+    """The time-chunked exchange of the multi-GPU path (kfp_swr_iterate_chunk + kfp_swr_chunk_send_wait /
+    _recv_done; dist.py), emulated on one device: two problems holding the two halves of the subdomains on
+    one compute stream, device-to-device copies of each chunk's edge rows on a second (communication)
+    stream standing in for NCCL.  No host synchronisation between chunks or iterations: the events alone
+    order the copies after the rows are written and the next iteration's chunk after its rows arrived.
+    Bitwise the single-process solve."""
+    import torch
+
+    run = ki.scaled(ki.config("c4"), nx=64, nv=16 * 64, nt=50, K=4, name="split").with_(n_sub=16)
+    prob = ki.make_problem(run)
+    full = _gpu(kfp, run)
+    cs, comm = torch.cuda.Stream(), torch.cuda.Stream()
+    A, B = kfp.Problem(prob), kfp.Problem(prob)
+    for pb_ in (A, B):
+        pb_.set_stream(cs.cuda_stream)
+    A.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, 0, 8)
+    B.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, 8, 16)
+    nt = run.grid.nt
+    shape = (nt, run.grid.nx)
+    bufs = {key: [torch.zeros(shape, dtype=torch.float64, device="cuda") for _ in range(2)]
+            for key in ("a_send", "a_recv", "b_send", "b_recv")}
+    for par in (0, 1):
+        A.bind_edge_buffers(par, send_right=bufs["a_send"][par].data_ptr(), recv_right=bufs["a_recv"][par].data_ptr())
+        B.bind_edge_buffers(par, send_left=bufs["b_send"][par].data_ptr(), recv_left=bufs["b_recv"][par].data_ptr())
+    torch.cuda.synchronize()
+    for k in range(1, run.K + 1):
+        par = k & 1
+        for c in range(nchunks):
+            A.iterate_chunk(c, nchunks)
+            B.iterate_chunk(c, nchunks)
+            n0, n1 = c * nt // nchunks, (c + 1) * nt // nchunks
+            with torch.cuda.stream(comm):
+                A.chunk_send_wait(comm.cuda_stream, c)
+                B.chunk_send_wait(comm.cuda_stream, c)
+                bufs["b_recv"][par][n0:n1].copy_(bufs["a_send"][par][n0:n1])  # stands in for NCCL send/recv
+                bufs["a_recv"][par][n0:n1].copy_(bufs["b_send"][par][n0:n1])
+                A.chunk_recv_done(comm.cuda_stream, c)
+                B.chunk_recv_done(comm.cuda_stream, c)
+    torch.cuda.synchronize()
+    eTa, eIa = A.history()
+    eTb, eIb = B.history()
+    assert np.array_equal(np.maximum(eTa, eTb), full["err_T"])
+    assert np.array_equal(np.maximum(eIa, eIb), full["err_if"])
+    for s in range(16):
+        assert np.array_equal((A if s < 8 else B).subdomain_uT(s), full["uT_sub"][s]), s
+    with pytest.raises(kfp.KfpError):  # chunks out of order
+        A.iterate_chunk(1, 4)
+    A.close()
+    B.close()
+
+
 def test_c2_full_size_vs_mode_reduced_oracle(kfp):
     """BASELINE.json configs[2] at full size (the bench workload, same launch plan), against the
     mode-reduced oracle (exact for the manufactured data, oracle/modal.py): every output element."""
