@@ -301,6 +301,28 @@ kfp_status kfp_swr_subdomain_range(kfp_problem pb, int32_t s, int32_t *lo, int32
  * i+1 (used at hi_i), dir 1 = sent rightwards by i (used at lo_{i+1}). */
 kfp_status kfp_swr_trace(kfp_problem pb, int32_t i, int32_t dir, double *out);
 
+/* x-sharded monodomain reference (multi-GPU; BJ.ns (c)).  A job of g processes computes the
+ * reference once instead of g times: this process solves only the columns [x0, x1) (whole 32-column tiles:
+ * x0 % 32 == 0, x1 % 32 == 0 or x1 == nx), recording U at the node lines[0..nlines) on those columns.  The
+ * upwind transport couples a column to its x-neighbours only, so after every kfp_monodomain_shard_step the
+ * caller moves send_lo (column x0 of u^{n+1}, all nv+1 nodes) to the process owning column x0 - 1 and
+ * send_hi (column x1 - 1) to the one owning x1 (periodic in x), into their recv_hi / recv_lo, on the
+ * problem's stream, before the next step; all four are caller-owned device buffers of nv+1 doubles (NULL
+ * allowed for the full range [0, nx), which needs no exchange).  shard_end completes the reference: U(T) and
+ * the U-lines are then valid on [x0, x1) only; the caller fills the other columns of the rows it needs
+ * with kfp_monodomain_shard_copy (dir 0: rows [r0, r1) x columns [xa, xb) of U(T) (what 0, node rows) or
+ * of the U-lines (what 1, row = line * nt + step) -> the contiguous device buffer buf [(r1-r0)][(xb-xa)];
+ * dir 1: buf -> the reference), after which kfp_swr_setup uses it like its own reference (its lines must
+ * be among `lines`).  Bitwise the unsharded reference on every column.  Errors: KFP_E_INVAL for a bad range,
+ * missing halo buffers, the split-FEM scheme with a partial range or bad copy bounds; KFP_E_STATE for steps
+ * outside [0, nt), shard_end before nt steps, a copy without a reference. */
+kfp_status kfp_monodomain_shard_begin(kfp_problem pb, int32_t x0, int32_t x1, const int32_t *lines, int32_t nlines,
+                                      double *send_lo, double *send_hi, double *recv_lo, double *recv_hi);
+kfp_status kfp_monodomain_shard_step(kfp_problem pb);
+kfp_status kfp_monodomain_shard_end(kfp_problem pb);
+kfp_status kfp_monodomain_shard_copy(kfp_problem pb, int32_t what, int32_t dir, int32_t r0, int32_t r1, int32_t xa,
+                                     int32_t xb, double *buf);
+
 /* Copy the monodomain U(T) [(nv+1)*nx] to host memory. */
 kfp_status kfp_monodomain_uT(kfp_problem pb, double *out);
 

@@ -192,6 +192,21 @@ bool make_tmap(CUtensorMap *map, double *rows_base, int nx, int nrows, int L, in
 }
 }  // namespace
 
+struct MonoRun {  // an in-progress monodomain reference (run_monodomain, kfp_monodomain_shard_*)
+    bool active = false, sharded = false;
+    int x0 = 0, x1 = 0, n = 0;
+    Plan pl;
+    SubDev sd;
+    SubDev *d_sd = nullptr;
+    StepParams P;
+    FusedData fd;
+    std::vector<double *> tmp;
+    std::vector<void *> tmp2;
+    int *d_rec = nullptr;
+    std::vector<int> rec_rows, lines;
+    double *halo[4] = {nullptr, nullptr, nullptr, nullptr};  // caller's send_lo, send_hi, recv_lo, recv_hi
+};
+
 struct kfp_problem_s {
     int device = 0;
     cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -253,6 +268,7 @@ struct kfp_problem_s {
     std::vector<double *> zero_on_reset;  // parity-0 incoming buffers
 
     int64_t launches = 0;
+    MonoRun mr;
     // time-chunked iterations (kfp_swr_iterate_chunk): per chunk, "outgoing rows written" and "incoming rows
     // arrived" events; the next chunk expected
     int nchunks = 0, chunk_next = 0;
@@ -445,14 +461,16 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
     P.b = pl.b;
     P.R = pl.R;
     P.C = pl.C;
-    const int ntiles = (pb->nx + kfp::kWarp - 1) / kfp::kWarp;
+    // x-tiles [tile0, tile_end) of this launch: every tile, or a sharded monodomain's column range
+    if (P.xend <= 0) P.xend = pb->nx;
+    const int tile_end = (P.xend + kfp::kWarp - 1) / kfp::kWarp, ntiles = tile_end - P.tile0;
     const dim3 block(pl.P * kfp::kWarp);
     if (pl.fused) {
         kfp::FusedParams FP;
         FP.S = P;
         FP.tmaps = fd.maps;
         FP.L = pl.L;
-        FP.ntiles = ntiles;
+        FP.ntiles = tile_end;  // (absolute: clusters walk t = tile0 + y, + Gc, ... < tile_end)
         FP.Gc = std::max(1, std::min(ntiles, pl.Gc_total / std::max(1, nsub)));
         FP.nrec = nrec;
         FP.rec_rows = rec_rows;
@@ -484,7 +502,7 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
     } else {
         kfp::step_phase1<<<dim3(pl.C, ntiles, nsub), block, pl.smem, pb->stream>>>(P);
         // phase 2: a warp per column (block recurrences as shuffle scans; step_phase2 is the serial reference form)
-        kfp::step_phase2_warp<<<dim3((pb->nx + 3) / 4, 1, nsub), 128, 0, pb->stream>>>(P);
+        kfp::step_phase2_warp<<<dim3((P.xend - P.tile0 * kfp::kWarp + 3) / 4, 1, nsub), 128, 0, pb->stream>>>(P);
         kfp::step_phase3<<<dim3(pl.C, ntiles, nsub), block, pl.smem, pb->stream>>>(P);
         pb->launches += 3;
     }
@@ -712,7 +730,11 @@ const double *final_slab(const kfp_problem pb, size_t ii) {
 }
 
 // Monodomain solve recording U at `lines` (BJ north_star (c)).
-kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
+// Monodomain reference in three pieces (mono_begin / mono_step / mono_end) so that a multi-GPU job can shard
+// it along x: each process computes the columns [x0, x1) and exchanges the halo columns x0 - 1 and x1 (the
+// upwind transport's only coupling between columns) after every step (kfp_monodomain_shard_*).
+kfp_status mono_begin(kfp_problem pb, const std::vector<int> &lines, int x0, int x1, double *const halo[4]) {
+    MonoRun &mr = pb->mr;
     const size_t nx = pb->nx, nn = (size_t)pb->nv + 1;
     if (!pb->d_mono[0]) {
         for (int q = 0; q < 2; ++q)
@@ -723,6 +745,7 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     std::vector<int> lon(nn, -1);
     for (size_t i = 0; i < lines.size(); ++i) lon[lines[i]] = (int)i;
     KFP_CUDA(cudaMemcpyAsync(pb->d_line_of_node, lon.data(), nn * sizeof(int), cudaMemcpyHostToDevice, pb->stream));
+    KFP_CUDA(cudaStreamSynchronize(pb->stream));  // (lon is a host temporary)
     if (pb->d_Ulines) {
         cudaFree(pb->d_Ulines);
         pb->allocs.erase(std::find(pb->allocs.begin(), pb->allocs.end(), (void *)pb->d_Ulines));
@@ -730,8 +753,9 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     }
     if (!lines.empty())
         if (kfp_status st = dalloc(pb, &pb->d_Ulines, lines.size() * (size_t)pb->nt * nx)) return st;
+    pb->mono_done = false;
 
-    SubDev sd;
+    SubDev &sd = mr.sd;
     std::memset(&sd, 0, sizeof sd);
     const bool fem = pb->scheme == KFP_SCHEME_SPLIT_FEM;
     sd.lo = 0;
@@ -744,7 +768,8 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     sd.slab[0] = pb->d_mono[0];
     sd.slab[1] = pb->d_mono[1];
     woodbury(pb, sd, 0.0, 0.0);
-    Plan pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true, fem);
+    mr.pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true, fem);
+    Plan &pl = mr.pl;
     if (fem && !pl.fused) {
         set_err("monodomain: the split-FEM scheme needs the cluster kernel (column of %d rows > %d)", sd.n, 8 * 16 * 33);
         return KFP_E_INVAL;
@@ -752,48 +777,97 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
     sd.nblk = (sd.n + pl.R - 1) / pl.R;
     if (kfp_status st = ensure_qtab(pb, std::max(pl.R, sd.n) + 2)) return st;
     if (kfp_status st = configure_kernels(pl)) return st;
-    SubDev *d_sd = nullptr;
-    std::vector<double *> tmp;
-    KFP_CUDA(cudaMalloc(&d_sd, sizeof(SubDev)));
-    KFP_CUDA(cudaMemcpyAsync(d_sd, &sd, sizeof sd, cudaMemcpyHostToDevice, pb->stream));
-    StepParams P = base_params(pb);
-    P.subs = d_sd;
+    KFP_CUDA(cudaMalloc(&mr.d_sd, sizeof(SubDev)));
+    KFP_CUDA(cudaMemcpyAsync(mr.d_sd, &sd, sizeof sd, cudaMemcpyHostToDevice, pb->stream));
+    StepParams &P = mr.P;
+    P = base_params(pb);
+    P.subs = mr.d_sd;
     P.record = lines.empty() ? 0 : 1;
     P.line_of_node = pb->d_line_of_node;
     P.rec = pb->d_Ulines;
     P.last = 0;  // no error accumulation on the reference itself; end rows stay 0 (memset)
-    std::vector<void *> tmp2;
-    FusedData fd;
-    int *d_rec = nullptr;
-    std::vector<int> rec_rows(lines.size());
-    for (size_t i = 0; i < lines.size(); ++i) rec_rows[i] = lines[i] - sd.first;
-    kfp_status st = alloc_general_scratch(pb, pl, 1, &P.blkagg, &P.chkagg, &P.carry, tmp);
-    if (!st) st = build_tmaps(pb, pl, std::vector<SubDev>{sd}, &fd.maps, &tmp2);
-    if (!st) st = build_l2m(pb, pl, std::vector<SubDev>{sd}, &fd.l2c, &tmp2);
-    if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &fd.coefT, &fd.tabs, &tmp2);
-    if (!st && !rec_rows.empty()) {
-        if (cudaMalloc(&d_rec, sizeof(int) * rec_rows.size()) != cudaSuccess ||
-            cudaMemcpy(d_rec, rec_rows.data(), sizeof(int) * rec_rows.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    P.tile0 = x0 / kfp::kWarp;
+    P.xend = x1;
+    mr.rec_rows.assign(lines.size(), 0);
+    for (size_t i = 0; i < lines.size(); ++i) mr.rec_rows[i] = lines[i] - sd.first;
+    kfp_status st = alloc_general_scratch(pb, pl, 1, &P.blkagg, &P.chkagg, &P.carry, mr.tmp);
+    if (!st) st = build_tmaps(pb, pl, std::vector<SubDev>{sd}, &mr.fd.maps, &mr.tmp2);
+    if (!st) st = build_l2m(pb, pl, std::vector<SubDev>{sd}, &mr.fd.l2c, &mr.tmp2);
+    if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &mr.fd.coefT, &mr.fd.tabs, &mr.tmp2);
+    if (!st && !mr.rec_rows.empty()) {
+        if (cudaMalloc(&mr.d_rec, sizeof(int) * mr.rec_rows.size()) != cudaSuccess ||
+            cudaMemcpy(mr.d_rec, mr.rec_rows.data(), sizeof(int) * mr.rec_rows.size(), cudaMemcpyHostToDevice) != cudaSuccess)
             st = KFP_E_CUDA;
     }
-    for (int n = 0; st == KFP_OK && n < pb->nt; ++n)
-        st = launch_step(pb, pl, P, 1, n, fd, (int)rec_rows.size(), d_rec);
-    if (st == KFP_OK && fem) {  // U(T): the last Step 2 (no error slot)
+    mr.x0 = x0;
+    mr.x1 = x1;
+    mr.n = 0;
+    mr.lines = lines;
+    mr.sharded = !(x0 == 0 && x1 == pb->nx);
+    for (int k = 0; k < 4; ++k) mr.halo[k] = halo ? halo[k] : nullptr;
+    mr.active = true;
+    return st;
+}
+
+void mono_free(kfp_problem pb) {
+    MonoRun &mr = pb->mr;
+    if (mr.d_sd) cudaFree(mr.d_sd);
+    if (mr.d_rec) cudaFree(mr.d_rec);
+    for (double *q : mr.tmp) cudaFree(q);
+    for (void *q : mr.tmp2) cudaFree(q);
+    mr = MonoRun();
+}
+
+kfp_status mono_step(kfp_problem pb) {
+    MonoRun &mr = pb->mr;
+    const int n = mr.n, nx = pb->nx, rows = pb->nv + 1;
+    const unsigned gb = (unsigned)((rows + 255) / 256);
+    if (mr.sharded && n > 0) {  // the halo columns of u^n from the neighbouring shards
+        kfp::halo_unpack<<<gb, 256, 0, pb->stream>>>(pb->d_mono[n & 1], nx, rows, (mr.x0 - 1 + nx) % nx, mr.halo[2]);
+        kfp::halo_unpack<<<gb, 256, 0, pb->stream>>>(pb->d_mono[n & 1], nx, rows, mr.x1 % nx, mr.halo[3]);
+        pb->launches += 2;
+    }
+    if (kfp_status st = launch_step(pb, mr.pl, mr.P, 1, n, mr.fd, (int)mr.rec_rows.size(), mr.d_rec)) return st;
+    if (mr.sharded) {  // this shard's edge columns of u^{n+1} for the neighbours
+        kfp::halo_pack<<<gb, 256, 0, pb->stream>>>(pb->d_mono[(n + 1) & 1], nx, rows, mr.x0, mr.halo[0]);
+        kfp::halo_pack<<<gb, 256, 0, pb->stream>>>(pb->d_mono[(n + 1) & 1], nx, rows, mr.x1 - 1, mr.halo[1]);
+        pb->launches += 2;
+        KFP_CUDA(cudaGetLastError());
+    }
+    mr.n = n + 1;
+    return KFP_OK;
+}
+
+kfp_status mono_end(kfp_problem pb) {
+    MonoRun &mr = pb->mr;
+    kfp_status st = KFP_OK;
+    if (pb->scheme == KFP_SCHEME_SPLIT_FEM) {  // U(T): the last Step 2 (no error slot)
+        StepParams P = mr.P;
         P.UT = nullptr;
         P.errT = nullptr;
         st = launch_fem_finish(pb, P, 1, pb->nv + 1);
     }
     cudaError_t e = cudaStreamSynchronize(pb->stream);
-    cudaFree(d_sd);
-    if (d_rec) cudaFree(d_rec);
-    for (double *q : tmp) cudaFree(q);
-    for (void *q : tmp2) cudaFree(q);
+    const std::vector<int> lines = mr.lines;
+    mono_free(pb);
     if (st != KFP_OK) return st;
     KFP_CUDA(e);
     pb->d_UT = pb->d_mono[final_parity(pb)];
     pb->mono_lines = lines;
     pb->mono_done = true;
     return KFP_OK;
+}
+
+kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
+    if (pb->mr.active) mono_free(pb);
+    kfp_status st = mono_begin(pb, lines, 0, pb->nx, nullptr);
+    for (int n = 0; st == KFP_OK && n < pb->nt; ++n) st = mono_step(pb);
+    if (st != KFP_OK) {
+        cudaStreamSynchronize(pb->stream);
+        mono_free(pb);
+        return st;
+    }
+    return mono_end(pb);
 }
 
 }  // namespace
@@ -928,6 +1002,7 @@ void kfp_problem_destroy(kfp_problem pb) {
     if (!pb) return;
     cudaSetDevice(pb->device);
     if (pb->stream) cudaStreamSynchronize(pb->stream);
+    if (pb->mr.active) mono_free(pb);
     free_swr(pb);
     for (void *p : pb->allocs) cudaFree(p);
     for (cudaEvent_t e : pb->ev) cudaEventDestroy(e);
@@ -959,6 +1034,86 @@ kfp_status kfp_monodomain_solve(kfp_problem pb, double *uT) {
                                  pb->stream));
         KFP_CUDA(cudaStreamSynchronize(pb->stream));
     }
+    return KFP_OK;
+}
+
+kfp_status kfp_monodomain_shard_begin(kfp_problem pb, int32_t x0, int32_t x1, const int32_t *lines, int32_t nlines,
+                                      double *send_lo, double *send_hi, double *recv_lo, double *recv_hi) {
+    if (!pb || nlines < 0 || (nlines > 0 && !lines)) {
+        set_err("kfp_monodomain_shard_begin: NULL problem or lines");
+        return KFP_E_INVAL;
+    }
+    const bool full = (x0 == 0 && x1 == pb->nx);
+    if (x0 < 0 || x1 > pb->nx || x0 >= x1 || x0 % kfp::kWarp || (x1 % kfp::kWarp && x1 != pb->nx)) {
+        set_err("kfp_monodomain_shard_begin: columns [%d, %d) must be a range of 32-column tiles of [0, %d)", x0, x1, pb->nx);
+        return KFP_E_INVAL;
+    }
+    if (!full && (!send_lo || !send_hi || !recv_lo || !recv_hi)) {
+        set_err("kfp_monodomain_shard_begin: a partial column range needs the four halo buffers");
+        return KFP_E_INVAL;
+    }
+    if (!full && pb->scheme == KFP_SCHEME_SPLIT_FEM) {
+        set_err("kfp_monodomain_shard_begin: the split-FEM reference is not sharded");
+        return KFP_E_INVAL;
+    }
+    std::vector<int> ls(lines, lines + nlines);
+    for (int l : ls)
+        if (l < 0 || l > pb->nv) {
+            set_err("kfp_monodomain_shard_begin: line node %d outside [0, %d]", l, pb->nv);
+            return KFP_E_INVAL;
+        }
+    KFP_CUDA(cudaSetDevice(pb->device));
+    if (pb->mr.active) mono_free(pb);
+    double *halo[4] = {send_lo, send_hi, recv_lo, recv_hi};
+    if (kfp_status st = mono_begin(pb, ls, x0, x1, halo)) {
+        cudaStreamSynchronize(pb->stream);
+        mono_free(pb);
+        return st;
+    }
+    return KFP_OK;
+}
+
+kfp_status kfp_monodomain_shard_step(kfp_problem pb) {
+    if (!pb || !pb->mr.active || pb->mr.n >= pb->nt) {
+        set_err("kfp_monodomain_shard_step: no sharded reference in progress (or all %d steps done)", pb ? pb->nt : 0);
+        return KFP_E_STATE;
+    }
+    KFP_CUDA(cudaSetDevice(pb->device));
+    return mono_step(pb);
+}
+
+kfp_status kfp_monodomain_shard_end(kfp_problem pb) {
+    if (!pb || !pb->mr.active || pb->mr.n != pb->nt) {
+        set_err("kfp_monodomain_shard_end: the reference has not run its %d steps", pb ? pb->nt : 0);
+        return KFP_E_STATE;
+    }
+    KFP_CUDA(cudaSetDevice(pb->device));
+    return mono_end(pb);
+}
+
+kfp_status kfp_monodomain_shard_copy(kfp_problem pb, int32_t what, int32_t dir, int32_t r0, int32_t r1, int32_t xa,
+                                     int32_t xb, double *buf) {
+    if (!pb || !buf || (what != 0 && what != 1) || (dir != 0 && dir != 1)) {
+        set_err("kfp_monodomain_shard_copy: bad arguments");
+        return KFP_E_INVAL;
+    }
+    if (!pb->mono_done || (what == 1 && !pb->d_Ulines)) {
+        set_err("kfp_monodomain_shard_copy: no reference (or no recorded lines)");
+        return KFP_E_STATE;
+    }
+    const int rows = what == 0 ? pb->nv + 1 : (int)pb->mono_lines.size() * pb->nt;
+    if (r0 < 0 || r1 > rows || r0 > r1 || xa < 0 || xb > pb->nx || xa > xb) {
+        set_err("kfp_monodomain_shard_copy: rows [%d, %d) of %d / columns [%d, %d) of %d", r0, r1, rows, xa, xb, pb->nx);
+        return KFP_E_INVAL;
+    }
+    if (r0 == r1 || xa == xb) return KFP_OK;
+    KFP_CUDA(cudaSetDevice(pb->device));
+    double *base = (what == 0 ? pb->d_UT : pb->d_Ulines) + (size_t)r0 * pb->nx + xa;
+    const size_t w = (size_t)(xb - xa) * sizeof(double), pitch = (size_t)pb->nx * sizeof(double);
+    if (dir == 0)
+        KFP_CUDA(cudaMemcpy2DAsync(buf, w, base, pitch, w, r1 - r0, cudaMemcpyDefault, pb->stream));
+    else
+        KFP_CUDA(cudaMemcpy2DAsync(base, pitch, buf, w, w, r1 - r0, cudaMemcpyDefault, pb->stream));
     return KFP_OK;
 }
 

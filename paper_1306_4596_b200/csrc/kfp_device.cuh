@@ -85,6 +85,7 @@ struct StepParams {
     int f_rank, u0_rank;
     int P, b, R, C;        // warps per CTA, rows per chunk, rows per block, blocks per column
     int qtab_len;
+    int tile0, xend;       // x-columns [32 tile0, xend) of this launch (a sharded monodomain); 0, nx otherwise
     int record;            // monodomain: record rows listed in line_of_node
     int ovrec;             // record the overlap rows into SubDev::ovb (cluster kernel only)
     double q, a, qa, hv, dt, p;   // split FEM: a = tau/h_v^2 - 1/6, dt = tau
@@ -172,6 +173,18 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
+// ------------------------------------------------------------------ sharded monodomain halo columns
+// Column m of every node row of a node-major slab [(nv+1)][nx] <-> a contiguous [(nv+1)] buffer (the x-halo of
+// an x-sharded monodomain reference, exchanged between processes every step).  grid ceil((nv+1)/256).
+__global__ void __launch_bounds__(256) halo_pack(const double *slab, int nx, int rows, int m, double *out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < rows) out[j] = slab[static_cast<size_t>(j) * nx + m];
+}
+__global__ void __launch_bounds__(256) halo_unpack(double *slab, int nx, int rows, int m, const double *in) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < rows) slab[static_cast<size_t>(j) * nx + m] = in[j];
+}
+
 // ------------------------------------------------------------------ geometry of one CTA
 struct Tile {
     const SubDev *sd;
@@ -188,8 +201,8 @@ __device__ __forceinline__ Tile make_tile(const StepParams &P, int blk) {
     Tile t;
     t.sub = blockIdx.z;
     t.sd = P.subs + t.sub;
-    t.m0 = blockIdx.y * kWarp;
-    t.w = min(kWarp, P.nx - t.m0);
+    t.m0 = (P.tile0 + blockIdx.y) * kWarp;
+    t.w = min(kWarp, P.xend - t.m0);
     t.blk = blk;
     t.rb0 = blk * P.R;
     t.Rb = max(0, min(P.R, t.sd->n - t.rb0));
@@ -723,9 +736,9 @@ __device__ __forceinline__ void p2w_sweep(const StepParams &P, int sub, int m, i
 }
 
 __global__ void __launch_bounds__(128) step_phase2_warp(const StepParams P) {
-    const int lane = threadIdx.x & 31, m = blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+    const int lane = threadIdx.x & 31, m = P.tile0 * kWarp + blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
     const int sub = blockIdx.z;
-    if (m >= P.nx) return;  // a whole warp per column
+    if (m >= P.xend) return;  // a whole warp per column
     const SubDev &S = P.subs[sub];
     const int nblk = S.nblk, n = S.n;
     const int brow[4] = {0, 1, n - 2, n - 1};

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
 #endif
 #pragma unroll
     for (int qq = 4; qq < 6; ++qq) cta_special |= inblk(sp_row[qq]);
-    const int t_first = blockIdx.y;
+    const int t_first = P.tile0 + blockIdx.y;  // (a sharded monodomain starts at tile0; ntiles = its end)
     const uint32_t tile_bytes = static_cast<uint32_t>(kTW * (L + 2 * kX) * sizeof(double));
     // tensor-map row of the tile's first row: FD maps start at the first unknown row, FEM maps at the
     // slab's first node (the row above the chunk may be a Dirichlet end node)

@@ -38,11 +38,90 @@ def block_of(rank: int, world: int, n_sub: int):
     return rank * per, (rank + 1) * per
 
 
+def decompose(nv: int, n_sub: int, overlap: int):
+    """Subdomain node ranges [lo_s, hi_s] (R9: split nodes s nv / S, the overlap placed with
+    floor(ov/2) nodes below and ceil(ov/2) above each split) -- the same ranges kfp_swr_setup uses."""
+    c = [s * (nv // n_sub) for s in range(n_sub + 1)]
+    lo = [0 if s == 0 else c[s] - overlap // 2 for s in range(n_sub)]
+    hi = [nv if s == n_sub - 1 else c[s + 1] + (overlap + 1) // 2 for s in range(n_sub)]
+    return lo, hi
+
+
+def column_range(rank: int, world: int, nx: int):
+    """This rank's x-columns of the sharded monodomain reference: a contiguous run of whole 32-column tiles."""
+    ntiles = (nx + 31) // 32
+    t0, t1 = rank * ntiles // world, (rank + 1) * ntiles // world
+    return t0 * 32, min(nx, t1 * 32)
+
+
+def sharded_monodomain(pb, grid, n_sub: int, overlap: int, rank: int, world: int, device):
+    """The monodomain reference computed ONCE by the whole job: rank r solves the columns
+    column_range(r) with a one-column halo exchanged with its x-neighbours after every step (NCCL P2P), then
+    every rank receives, from every other, the columns it lacks of the U(T) rows of its own subdomains and of
+    its interface lines (one all-to-all of point-to-point pairs).  Afterwards kfp_swr_setup finds the reference in place."""
+    nx, nv, nt = grid.nx, grid.nv, grid.nt
+    lo, hi = decompose(nv, n_sub, overlap)
+    lines = sorted({lo[s] for s in range(1, n_sub)} | {hi[s] for s in range(n_sub - 1)})
+    x0, x1 = column_range(rank, world, nx)
+    rows = nv + 1
+    halo = [torch.empty(rows, dtype=torch.float64, device=device) for _ in range(4)]
+    pb.mono_shard_begin(x0, x1, lines, halo)
+    left, right = (rank - 1) % world, (rank + 1) % world
+    for _ in range(nt):
+        pb.mono_shard_step()
+        # column x1-1 to the right neighbour, column x0 to the left one; their edge columns back.  Sends
+        # and receives in this order so that with two ranks (left == right) each receive pairs with the
+        # matching send of the peer.
+        ops = [dist.P2POp(dist.isend, halo[1], right), dist.P2POp(dist.isend, halo[0], left),
+               dist.P2POp(dist.irecv, halo[2], left), dist.P2POp(dist.irecv, halo[3], right)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    pb.mono_shard_end()
+    # what each rank needs: the U(T) node rows of its subdomains, the U-line rows of its interface lines
+    need = []
+    for r in range(world):
+        sb, se = block_of(r, world, n_sub)
+        ranges = [(0, lo[sb], hi[se - 1] + 1)]
+        for s in range(sb, se):
+            for node in ([lo[s]] if s > 0 else []) + ([hi[s]] if s < n_sub - 1 else []):
+                li = lines.index(node)
+                ranges.append((1, li * nt, (li + 1) * nt))
+        need.append(ranges)
+    cols = [column_range(r, world, nx) for r in range(world)]
+    nrows = lambda rg: sum(b - a for _, a, b in rg)
+    send = [torch.empty((nrows(need[r]), x1 - x0), dtype=torch.float64, device=device) for r in range(world)]
+    for r in range(world):
+        if r == rank:
+            continue
+        off = 0
+        for what, a, b in need[r]:
+            pb.mono_shard_copy(what, 0, a, b, x0, x1, send[r][off:off + b - a])
+            off += b - a
+    recv = [torch.empty((nrows(need[rank]), cols[r][1] - cols[r][0]), dtype=torch.float64, device=device)
+            for r in range(world)]
+    ops = []  # the all-to-all as point-to-point pairs (NCCL and gloo alike)
+    for r in range(world):
+        if r != rank:
+            ops.append(dist.P2POp(dist.isend, send[r], r))
+            ops.append(dist.P2POp(dist.irecv, recv[r], r))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for r in range(world):
+        if r == rank:
+            continue
+        off = 0
+        for what, a, b in need[rank]:
+            pb.mono_shard_copy(what, 1, a, b, cols[r][0], cols[r][1], recv[r][off:off + b - a])
+            off += b - a
+    return lines
+
+
 class CudaBlock:
     """The local block on this rank's GPU, through the C-ABI (libkfp.so)."""
 
     def __init__(self, prob, kind: str, p: float, overlap: int, n_sub: int, K: int, rank: int, world: int,
-                 device: int, q=None, stream=None):
+                 device: int, q=None, stream=None, shard_reference: bool = True):
         from .kfp import Problem
 
         self.s_begin, self.s_end = block_of(rank, world, n_sub)
@@ -57,6 +136,8 @@ class CudaBlock:
         torch.cuda.set_stream(self.stream)
         self.pb = Problem(prob, device=device)
         self.pb.set_stream(self.stream.cuda_stream)
+        if shard_reference and world > 1 and getattr(prob, "scheme", "imex_fd") == "imex_fd":
+            sharded_monodomain(self.pb, g, n_sub, overlap, rank, world, f"cuda:{device}")
         self.pb.setup(kind, p, overlap, n_sub, K, self.s_begin, self.s_end, q=q)
         shape = (g.nt, g.nx)
         mk = lambda: torch.zeros(shape, dtype=torch.float64, device=f"cuda:{device}")

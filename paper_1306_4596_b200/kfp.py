@@ -29,6 +29,7 @@ SYMBOLS = (
     "kfp_plan", "kfp_last_timing", "kfp_last_error",
     "kfp_swr_set_overlap_error", "kfp_swr_overlap_history", "kfp_swr_iterate_until", "kfp_swr_set_pipeline",
     "kfp_swr_iterate_chunk", "kfp_swr_chunk_send_wait", "kfp_swr_chunk_recv_done",
+    "kfp_monodomain_shard_begin", "kfp_monodomain_shard_step", "kfp_monodomain_shard_end", "kfp_monodomain_shard_copy",
 )
 
 
@@ -98,6 +99,10 @@ def load(path: str = LIB_PATH):
         "kfp_swr_overlap_history": (i32, [vp, i32, i32, ctypes.POINTER(i32), vp]),
         "kfp_swr_iterate_until": (i32, [vp, i32, dbl, i32, ctypes.POINTER(i32)]),
         "kfp_swr_iterate_chunk": (i32, [vp, i32, i32]),
+        "kfp_monodomain_shard_begin": (i32, [vp, i32, i32, vp, i32, vp, vp, vp, vp]),
+        "kfp_monodomain_shard_step": (i32, [vp]),
+        "kfp_monodomain_shard_end": (i32, [vp]),
+        "kfp_monodomain_shard_copy": (i32, [vp, i32, i32, i32, i32, i32, i32, vp]),
         "kfp_swr_chunk_send_wait": (i32, [vp, vp, i32]),
         "kfp_swr_chunk_recv_done": (i32, [vp, vp, i32]),
     }
@@ -232,6 +237,27 @@ class Problem:
 
     def chunk_recv_done(self, stream_handle: int, chunk: int):
         _check(load().kfp_swr_chunk_recv_done(self._h, ctypes.c_void_p(stream_handle), int(chunk)))
+
+    def mono_shard_begin(self, x0: int, x1: int, lines, halo=(None, None, None, None)):
+        """x-sharded monodomain reference: columns [x0, x1); halo = (send_lo, send_hi, recv_lo, recv_hi), device
+        tensors or pointers of nv+1 doubles each (include/kfp.h)."""
+        arr = np.ascontiguousarray(lines, dtype=np.int32)
+        c = lambda p: None if p is None else ctypes.c_void_p(p if isinstance(p, int) else p.data_ptr())
+        _check(load().kfp_monodomain_shard_begin(self._h, int(x0), int(x1), _ptr(arr) if arr.size else None,
+                                                 int(arr.size), *[c(p) for p in halo]))
+
+    def mono_shard_step(self):
+        _check(load().kfp_monodomain_shard_step(self._h))
+
+    def mono_shard_end(self):
+        _check(load().kfp_monodomain_shard_end(self._h))
+
+    def mono_shard_copy(self, what: int, direction: int, r0: int, r1: int, xa: int, xb: int, buf):
+        """U(T) (what 0) / U-lines (what 1) rows [r0, r1) x columns [xa, xb) <-> a contiguous device buffer
+        (tensor or pointer) of (r1 - r0) x (xb - xa) doubles."""
+        ptr = buf if isinstance(buf, int) else buf.data_ptr()
+        _check(load().kfp_monodomain_shard_copy(self._h, int(what), int(direction), int(r0), int(r1), int(xa), int(xb),
+                                                ctypes.c_void_p(ptr)))
 
     def edge_buffers(self, parity: int):
         """(send_left, recv_left, send_right, recv_right) device pointers (int or None)."""

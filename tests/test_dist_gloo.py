@@ -172,3 +172,78 @@ def test_block_partition():
     assert [block_of(r, 8, 32) for r in range(8)] == [(4 * r, 4 * r + 4) for r in range(8)]
     with pytest.raises(ValueError):
         block_of(0, 3, 32)
+
+
+class FakeShardProblem:
+    """The library side of dist.sharded_monodomain on CPU (tests only): U(T) and the U-lines come from the
+    oracle's monodomain, with every column outside this rank's range poisoned (NaN) until the all_to_all
+    fills it; each step writes (rank, step, side) markers into the send halo and checks that the receive
+    halo holds the right neighbour's marker -- the exchange pattern of the x-halo, including two ranks where
+    the left and the right neighbour are the same process."""
+
+    def __init__(self, prob, rank, world):
+        self.prob, self.rank, self.world = prob, rank, world
+
+    def mono_shard_begin(self, x0, x1, lines, halo):
+        import oracle
+
+        self.x0, self.x1, self.halo, self.n = x0, x1, halo, 0
+        UT, rec = oracle.monodomain(self.prob, lines)
+        self.UT = UT.copy()
+        self.UL = rec.reshape(len(lines) * self.prob.grid.nt, self.prob.grid.nx).copy()
+        self.ref = (UT, rec.reshape(self.UL.shape).copy())
+        for a in (self.UT, self.UL):
+            a[:, :x0] = np.nan
+            a[:, x1:] = np.nan
+
+    def mono_shard_step(self):
+        if self.n > 0:  # recv_lo: the left neighbour's send_hi (side 1); recv_hi: the right one's send_lo (side 0)
+            left, right = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+            assert self.halo[2][0].item() == 1000 * left + 10 * (self.n - 1) + 1, (self.rank, self.halo[2][0])
+            assert self.halo[3][0].item() == 1000 * right + 10 * (self.n - 1) + 0, (self.rank, self.halo[3][0])
+        self.halo[0].fill_(1000 * self.rank + 10 * self.n + 0)
+        self.halo[1].fill_(1000 * self.rank + 10 * self.n + 1)
+        self.n += 1
+
+    def mono_shard_end(self):
+        pass
+
+    def mono_shard_copy(self, what, direction, a, b, xa, xb, buf):
+        arr = self.UT if what == 0 else self.UL
+        if direction == 0:
+            buf.copy_(torch.from_numpy(np.ascontiguousarray(arr[a:b, xa:xb])))
+        else:
+            arr[a:b, xa:xb] = buf.numpy()
+
+
+def _shard_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1306_4596_b200.dist import block_of, decompose, sharded_monodomain
+
+    run = ki.scaled(ki.config("c4"), nx=128, nv=64, nt=6, K=2).with_(n_sub=4)
+    prob = ki.make_problem(run)
+    pb = FakeShardProblem(prob, rank, world)
+    lines = sharded_monodomain(pb, run.grid, run.n_sub, run.overlap, rank, world, "cpu")
+    lo, hi = decompose(run.grid.nv, run.n_sub, run.overlap)
+    sb, se = block_of(rank, world, run.n_sub)
+    UT, UL = pb.ref
+    ok = np.array_equal(pb.UT[lo[sb]:hi[se - 1] + 1], UT[lo[sb]:hi[se - 1] + 1])
+    nt = run.grid.nt
+    for s in range(sb, se):
+        for node in ([lo[s]] if s > 0 else []) + ([hi[s]] if s < run.n_sub - 1 else []):
+            li = lines.index(node)
+            ok &= np.array_equal(pb.UL[li * nt:(li + 1) * nt], UL[li * nt:(li + 1) * nt])
+    out[rank] = bool(ok)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_monodomain_exchange(world):
+    """dist.sharded_monodomain's host logic (x-halo P2P every step, the all_to_all redistribution) with gloo:
+    every rank ends with the complete U(T) rows of its subdomains and its interface lines."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_shard_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert all(out[r] for r in range(world))

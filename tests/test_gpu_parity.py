@@ -212,6 +212,79 @@ def test_block_split_chunked_exchange(kfp, nchunks):
     B.close()
 
 
+@pytest.mark.parametrize("nv", [1024, 8192])
+def test_sharded_monodomain_reference(kfp, nv):
+    """The x-sharded monodomain reference of the multi-GPU path (kfp_monodomain_shard_*; dist.sharded_monodomain),
+    emulated on one device with two problems owning the x-columns [0, 64) and [64, 128): the halo columns move
+    by device copies after every step, then each problem receives the other's columns of its own U(T) rows
+    and interface lines (kfp_monodomain_shard_copy).  nv = 1024: cluster-kernel reference, 8192: three-phase
+    reference.  The two halves then run the split SWR solve (edge traces by copies) and must be bitwise the
+    single-process solve -- every err_T / err_if entry reads the reference."""
+    import torch
+
+    from paper_1306_4596_b200.dist import column_range, decompose
+
+    run = ki.scaled(ki.config("c4"), nx=128, nv=nv, nt=20, K=3, name="shard").with_(n_sub=8)
+    prob = ki.make_problem(run)
+    g = run.grid
+    full = _gpu(kfp, run)
+    cs = torch.cuda.Stream()
+    torch.cuda.set_stream(cs)
+    try:
+        lo, hi = decompose(g.nv, run.n_sub, run.overlap)
+        lines = sorted({lo[s] for s in range(1, run.n_sub)} | {hi[s] for s in range(run.n_sub - 1)})
+        P = [kfp.Problem(prob), kfp.Problem(prob)]
+        halo = [[torch.empty(g.nv + 1, dtype=torch.float64, device="cuda") for _ in range(4)] for _ in range(2)]
+        cols = [column_range(r, 2, g.nx) for r in range(2)]
+        for r in range(2):
+            P[r].set_stream(cs.cuda_stream)
+            P[r].mono_shard_begin(*cols[r], lines, halo[r])
+        for _ in range(g.nt):
+            for r in range(2):
+                P[r].mono_shard_step()
+            for r in range(2):  # recv_lo <- the other's send_hi, recv_hi <- the other's send_lo (periodic x)
+                halo[r][2].copy_(halo[1 - r][1])
+                halo[r][3].copy_(halo[1 - r][0])
+        for r in range(2):
+            P[r].mono_shard_end()
+        blocks = [(0, 4), (4, 8)]
+        for r in range(2):  # the other half's columns of this half's U(T) rows and interface lines
+            o = 1 - r
+            sb, se = blocks[r]
+            ranges = [(0, lo[sb], hi[se - 1] + 1)]
+            for s_ in range(sb, se):
+                for node in ([lo[s_]] if s_ > 0 else []) + ([hi[s_]] if s_ < run.n_sub - 1 else []):
+                    li = lines.index(node)
+                    ranges.append((1, li * g.nt, (li + 1) * g.nt))
+            for what, a, b in ranges:
+                buf = torch.empty((b - a, cols[o][1] - cols[o][0]), dtype=torch.float64, device="cuda")
+                P[o].mono_shard_copy(what, 0, a, b, *cols[o], buf)
+                P[r].mono_shard_copy(what, 1, a, b, *cols[o], buf)
+        shape = (g.nt, g.nx)
+        bufs = {key: [torch.zeros(shape, dtype=torch.float64, device="cuda") for _ in range(2)]
+                for key in ("a_send", "a_recv", "b_send", "b_recv")}
+        P[0].setup(run.kind, run.p, run.overlap, run.n_sub, run.K, 0, 4)
+        P[1].setup(run.kind, run.p, run.overlap, run.n_sub, run.K, 4, 8)
+        for par in (0, 1):
+            P[0].bind_edge_buffers(par, send_right=bufs["a_send"][par].data_ptr(), recv_right=bufs["a_recv"][par].data_ptr())
+            P[1].bind_edge_buffers(par, send_left=bufs["b_send"][par].data_ptr(), recv_left=bufs["b_recv"][par].data_ptr())
+        for k in range(1, run.K + 1):
+            P[0].iterate(1)
+            P[1].iterate(1)
+            bufs["b_recv"][k & 1].copy_(bufs["a_send"][k & 1])
+            bufs["a_recv"][k & 1].copy_(bufs["b_send"][k & 1])
+        torch.cuda.synchronize()
+        (eTa, eIa), (eTb, eIb) = P[0].history(), P[1].history()
+        assert np.array_equal(np.maximum(eTa, eTb), full["err_T"]), (eTa, eTb, full["err_T"])
+        assert np.array_equal(np.maximum(eIa, eIb), full["err_if"])
+        for s_ in range(run.n_sub):
+            assert np.array_equal(P[0 if s_ < 4 else 1].subdomain_uT(s_), full["uT_sub"][s_]), s_
+        for pb_ in P:
+            pb_.close()
+    finally:
+        torch.cuda.set_stream(torch.cuda.default_stream())
+
+
 def test_c2_full_size_vs_mode_reduced_oracle(kfp):
     """BASELINE.json configs[2] at full size (the bench workload, same launch plan), against the
     mode-reduced oracle (exact for the manufactured data, oracle/modal.py): every output element."""
