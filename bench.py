@@ -32,6 +32,7 @@ import numpy as np  # noqa: E402
 import kfp_inputs as ki  # noqa: E402
 
 BYTES_PER_UPDATE = 16  # read u^n + write u^{n+1}, fp64
+NOMINAL_HBM_GBS = 8000.0  # B200 datasheet HBM3e bandwidth (report both bases)
 
 
 def measured_peaks():
@@ -330,6 +331,7 @@ def bench_single(args):
                           "per-solve events)" % (slab_bytes / 1e6)),
                    "parallelism": "v-subdomains on 1 GPU", "updates_per_step": updates},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_nominal": NOMINAL_HBM_GBS, "frac_nominal": achieved / NOMINAL_HBM_GBS,
                      "traffic": traffic, "peak_kind": peak_kind, "kernel": "kfp::step_fused_tma",
                      "traffic_source": "profiles/*_ncu_summary.json (ncu --set full, same plan)" if traffic else None,
                      "bytes_per_launch": bytes_per_launch, "avg_launch_us": per_launch_s * 1e6},

@@ -111,3 +111,21 @@ def test_product_path_does_not_import_oracle():
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert "import paper_1306_4596_b200" not in txt and "from paper_1306_4596_b200" not in txt, f
             assert "libkfp" not in txt, f
+
+
+def test_new_calls_reject_null_without_device(lib):
+    """The round-2 calls validate their handle before any device work (no GPU needed): the chunked
+    iteration and its events, the sharded monodomain reference, and the non-finite status code."""
+    vp = ctypes.c_void_p
+    assert lib.kfp_swr_iterate_chunk(None, 0, 4) == -6           # KFP_E_STATE: no setup
+    assert lib.kfp_swr_chunk_send_wait(None, None, 0) == -1     # KFP_E_INVAL
+    assert lib.kfp_swr_chunk_recv_done(None, None, 0) == -1
+    assert lib.kfp_monodomain_shard_begin(None, 0, 32, None, 0, None, None, None, None) == -1
+    assert lib.kfp_monodomain_shard_step(None) == -6
+    assert lib.kfp_monodomain_shard_end(None) == -6
+    assert lib.kfp_monodomain_shard_copy(None, 0, 0, 0, 1, 0, 1, vp(1)) == -1
+    from paper_1306_4596_b200 import kfp
+
+    assert kfp.KFP_E_NONFINITE == -7
+    src = open(os.path.join(ROOT, "include", "kfp.h")).read()
+    assert "KFP_E_NONFINITE = -7" in src
