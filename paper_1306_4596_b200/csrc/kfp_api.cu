@@ -196,7 +196,7 @@ struct MonoRun {  // an in-progress monodomain reference (run_monodomain, kfp_mo
     bool active = false, sharded = false;
     int x0 = 0, x1 = 0, n = 0;
     Plan pl;
-    SubDev sd;
+    std::vector<SubDev> segs;  // the column, or its overlapping segments
     SubDev *d_sd = nullptr;
     StepParams P;
     FusedData fd;
@@ -755,30 +755,61 @@ kfp_status mono_begin(kfp_problem pb, const std::vector<int> &lines, int x0, int
         if (kfp_status st = dalloc(pb, &pb->d_Ulines, lines.size() * (size_t)pb->nt * nx)) return st;
     pb->mono_done = false;
 
-    SubDev &sd = mr.sd;
-    std::memset(&sd, 0, sizeof sd);
+    // The column [first, first + n) -- or, when it is taller than the cluster kernel's 8 x 16 x 33 rows (the
+    // c3 / c4 monodomain), overlapping segments of it.  A segment is solved as a column of its own with zero
+    // Dirichlet data just outside it and stores only its interior rows [wlo, whi); the artificial ends
+    // perturb the solution by ~ q^d / (1 - q^2) of its size at distance d (the discrete Green's function of
+    // tridiag(-a, 1 + 2a, -a) decays like q^d), so interiors H rows away with q^H / (1 - q^2) < 2^-60 are
+    // the column's solution to round-off.  (The FD scheme; the split-FEM reference stays one column.)
     const bool fem = pb->scheme == KFP_SCHEME_SPLIT_FEM;
-    sd.lo = 0;
-    sd.hi = pb->nv;
-    sd.first = fem ? 0 : 1;                 // FEM: Neumann ends, every node unknown
-    sd.n = fem ? pb->nv + 1 : pb->nv - 1;
-    sd.ltype = sd.rtype = fem ? kfp::END_NEU : kfp::END_PHYS;
-    sd.iL_tr = sd.iR_tr = -2;
-    sd.ifL = sd.ifR = -1;
-    sd.slab[0] = pb->d_mono[0];
-    sd.slab[1] = pb->d_mono[1];
-    woodbury(pb, sd, 0.0, 0.0);
-    mr.pl = make_plan(std::vector<int>{sd.n}, pb->f_rank, true, fem);
+    const int first = fem ? 0 : 1, ncol = fem ? pb->nv + 1 : pb->nv - 1;
+    auto column_sd = [&](int r0, int r1, int w0, int w1) {  // rows [r0, r1) of the column, stores [w0, w1)
+        SubDev sd;
+        std::memset(&sd, 0, sizeof sd);
+        sd.first = first + r0;
+        sd.n = r1 - r0;
+        sd.lo = sd.first - (fem ? 0 : 1);
+        sd.hi = sd.first + sd.n - (fem ? 1 : 0);
+        sd.ltype = sd.rtype = fem ? kfp::END_NEU : kfp::END_PHYS;
+        sd.iL_tr = sd.iR_tr = -2;
+        sd.ifL = sd.ifR = -1;
+        sd.slab[0] = pb->d_mono[0] + (size_t)sd.lo * nx;
+        sd.slab[1] = pb->d_mono[1] + (size_t)sd.lo * nx;
+        sd.wlo = w0 - r0;
+        sd.whi = w1 - r0;
+        woodbury(pb, sd, 0.0, 0.0);
+        return sd;
+    };
+    mr.segs.clear();
+    constexpr int kMaxCol = 8 * 16 * 33;  // the cluster kernel's tallest column
+    if (!fem && ncol > kMaxCol) {
+        const long double q = pb->q;
+        const int H = (int)std::ceil(std::log(std::ldexp(1.0L, -60) * (1.0L - q * q)) / std::log(q));
+        const int I = kMaxCol - 2 * H;  // interior rows per segment
+        if (I >= kMaxCol / 4)
+            for (int w0 = 0; w0 < ncol; w0 += I) {
+                const int w1 = std::min(ncol, w0 + I);
+                mr.segs.push_back(column_sd(std::max(0, w0 - H), std::min(ncol, w1 + H), w0, w1));
+            }
+    }
+    if (mr.segs.empty()) mr.segs.push_back(column_sd(0, ncol, 0, ncol));
+    std::vector<int> ns;
+    for (const SubDev &sd : mr.segs) ns.push_back(sd.n);
+    mr.pl = make_plan(ns, pb->f_rank, true, fem);
     Plan &pl = mr.pl;
     if (fem && !pl.fused) {
-        set_err("monodomain: the split-FEM scheme needs the cluster kernel (column of %d rows > %d)", sd.n, 8 * 16 * 33);
+        set_err("monodomain: the split-FEM scheme needs the cluster kernel (column of %d rows > %d)", ncol, kMaxCol);
         return KFP_E_INVAL;
     }
-    sd.nblk = (sd.n + pl.R - 1) / pl.R;
-    if (kfp_status st = ensure_qtab(pb, std::max(pl.R, sd.n) + 2)) return st;
+    int nmax = 0;
+    for (SubDev &sd : mr.segs) {
+        sd.nblk = (sd.n + pl.R - 1) / pl.R;
+        nmax = std::max(nmax, sd.n);
+    }
+    if (kfp_status st = ensure_qtab(pb, std::max(pl.R, nmax) + 2)) return st;
     if (kfp_status st = configure_kernels(pl)) return st;
-    KFP_CUDA(cudaMalloc(&mr.d_sd, sizeof(SubDev)));
-    KFP_CUDA(cudaMemcpyAsync(mr.d_sd, &sd, sizeof sd, cudaMemcpyHostToDevice, pb->stream));
+    KFP_CUDA(cudaMalloc(&mr.d_sd, sizeof(SubDev) * mr.segs.size()));
+    KFP_CUDA(cudaMemcpyAsync(mr.d_sd, mr.segs.data(), sizeof(SubDev) * mr.segs.size(), cudaMemcpyHostToDevice, pb->stream));
     StepParams &P = mr.P;
     P = base_params(pb);
     P.subs = mr.d_sd;
@@ -788,11 +819,10 @@ kfp_status mono_begin(kfp_problem pb, const std::vector<int> &lines, int x0, int
     P.last = 0;  // no error accumulation on the reference itself; end rows stay 0 (memset)
     P.tile0 = x0 / kfp::kWarp;
     P.xend = x1;
-    mr.rec_rows.assign(lines.size(), 0);
-    for (size_t i = 0; i < lines.size(); ++i) mr.rec_rows[i] = lines[i] - sd.first;
-    kfp_status st = alloc_general_scratch(pb, pl, 1, &P.blkagg, &P.chkagg, &P.carry, mr.tmp);
-    if (!st) st = build_tmaps(pb, pl, std::vector<SubDev>{sd}, &mr.fd.maps, &mr.tmp2);
-    if (!st) st = build_l2m(pb, pl, std::vector<SubDev>{sd}, &mr.fd.l2c, &mr.tmp2);
+    mr.rec_rows = lines;  // node indices (the cluster kernel converts per descriptor)
+    kfp_status st = alloc_general_scratch(pb, pl, (int)mr.segs.size(), &P.blkagg, &P.chkagg, &P.carry, mr.tmp);
+    if (!st) st = build_tmaps(pb, pl, mr.segs, &mr.fd.maps, &mr.tmp2);
+    if (!st) st = build_l2m(pb, pl, mr.segs, &mr.fd.l2c, &mr.tmp2);
     if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &mr.fd.coefT, &mr.fd.tabs, &mr.tmp2);
     if (!st && !mr.rec_rows.empty()) {
         if (cudaMalloc(&mr.d_rec, sizeof(int) * mr.rec_rows.size()) != cudaSuccess ||
@@ -827,7 +857,8 @@ kfp_status mono_step(kfp_problem pb) {
         kfp::halo_unpack<<<gb, 256, 0, pb->stream>>>(pb->d_mono[n & 1], nx, rows, mr.x1 % nx, mr.halo[3]);
         pb->launches += 2;
     }
-    if (kfp_status st = launch_step(pb, mr.pl, mr.P, 1, n, mr.fd, (int)mr.rec_rows.size(), mr.d_rec)) return st;
+    if (kfp_status st = launch_step(pb, mr.pl, mr.P, (int)mr.segs.size(), n, mr.fd, (int)mr.rec_rows.size(), mr.d_rec))
+        return st;
     if (mr.sharded) {  // this shard's edge columns of u^{n+1} for the neighbours
         kfp::halo_pack<<<gb, 256, 0, pb->stream>>>(pb->d_mono[(n + 1) & 1], nx, rows, mr.x0, mr.halo[0]);
         kfp::halo_pack<<<gb, 256, 0, pb->stream>>>(pb->d_mono[(n + 1) & 1], nx, rows, mr.x1 - 1, mr.halo[1]);

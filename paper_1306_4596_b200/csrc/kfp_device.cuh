@@ -66,8 +66,10 @@ struct SubDev {
     double *ovb[2];              // [ovn][nt][nx] this subdomain's values there (u; split FEM: w)
     // pipelined Jacobi iterations: this descriptor runs step P.n - lag of its
     // iteration; outside [0, nt) the CTA exits (pipeline fill / drain).  0 otherwise.
-    int lag, pad2_;
-    double pad3_;                // keep sizeof % 16 == 0 (the column kernel bulk-copies descriptor arrays)
+    int lag;
+    // rows [wlo, whi) of the column are stored (whi == 0: every row).  A tall monodomain column is solved as
+    // overlapping segments (kfp_api.cu mono_segments): each writes only its interior rows.
+    int wlo, whi, pad_;
 };
 static_assert(sizeof(SubDev) % 16 == 0, "SubDev arrays are copied with cp.async.bulk (16-B granules)");
 

@@ -47,7 +47,7 @@ struct FusedParams {
     int Gc;                       // clusters per subdomain (each walks the x-tiles t = y, y+Gc, ...)
     int ntiles;                   // 32-column x-tiles per subdomain
     int nrec;                     // monodomain line recording: number of recorded rows
-    const int *rec_rows;          // [nrec] unknown-row index of each recorded line (in line order)
+    const int *rec_rows;          // [nrec] node index of each recorded line (in line order)
     const double *l2m;            // [nsub][C][kL2M] level-2 linear maps (host-computed, kfp_api.cu)
     const double *coefT;          // [nv+1][2+NR] per-node (q/a)(1-|nu|), (q/a)|nu|, (q/a) fv_r(j)
     const double *tabs;           // qp[kQ] | s2[kQ] | kr[2B] for this plan (host-computed)
@@ -643,8 +643,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 for (int l = 0; l < B; ++l)
                     if (l < Lw) h[l] = fma(kap_s(qp, s2, l, Lw), Y, fma(qp[Lw - l], X, h[l]));
             }
+            const int wlo = S.wlo, whi = S.whi > 0 ? S.whi : n;  // rows this descriptor stores
             if (active) {
-                if (Lw == B) {  // full chunk: unpredicated global stores, one pointer step per row
+                if (Lw == B && cr0 >= wlo && cr0 + B <= whi) {  // full chunk: unpredicated stores, one pointer step per row
                     double *p = dst;
 #pragma unroll
                     for (int l = 0; l < B; ++l) {
@@ -654,7 +655,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 } else {
 #pragma unroll
                     for (int l = 0; l < B; ++l)
-                        if (l < Lw) dst[l * pitch] = h[l];
+                        if (l < Lw && cr0 + l >= wlo && cr0 + l < whi) dst[l * pitch] = h[l];
                 }
             }
             if (!FEM && last && active) {  // error at T on every unknown row (a 1/N_t fraction of the steps)
@@ -731,8 +732,8 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                     eif = nmax(eif, fabs(sm.xsp[5 * kWarp + lane] - P.Ulines[(static_cast<size_t>(S.ifR) * P.nt + step) * P.nx + m]));
                 if (P.record)  // read back this block's recorded rows of u^{n+1} (stored above by this CTA)
                     for (int i = 0; i < FP.nrec; ++i) {
-                        const int row = FP.rec_rows[i];
-                        if (inblk(row))
+                        const int row = FP.rec_rows[i] - S.first;  // (rec_rows: node indices)
+                        if (inblk(row) && row >= S.wlo && row < (S.whi > 0 ? S.whi : n))
                             P.rec[(static_cast<size_t>(i) * P.nt + step) * P.nx + m] = unew[static_cast<size_t>(row) * P.nx + m];
                     }
                 if (P.ovrec)  // this subdomain's overlap rows (unknown rows of this block; Dirichlet end nodes)

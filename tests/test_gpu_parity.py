@@ -60,8 +60,15 @@ def _compare(g, r, name):
     assert rel(g["uT"], r["uT"]) <= TOL, name
     for s, (a, b) in enumerate(zip(g["uT_sub"], r["uT_sub"])):
         assert rel(a, b) <= TOL, (name, s)
-    assert rel(g["err_T"], r["err_T"]) <= TOL, (name, g["err_T"], r["err_T"])
-    assert rel(g["err_if"], r["err_if"]) <= TOL, (name, g["err_if"], r["err_if"])
+    # a history that is identically zero (n_sub = 1: the iterate IS the reference) is compared on the scale of
+    # the solution (the two are separate computations -- e.g. a tall reference solved in overlapping segments --
+    # equal to round-off)
+    for e in ("err_T", "err_if"):
+        ref = np.asarray(r[e])
+        if np.abs(ref).max() == 0.0:
+            assert np.abs(np.asarray(g[e])).max() <= TOL * np.abs(r["UT"]).max(), (name, e, g[e])
+        else:
+            assert rel(g[e], ref) <= TOL, (name, e, g[e], ref)
     if r["traces"] is not None:
         for i, t in enumerate(g["traces"]):
             assert rel(t, r["traces"][i]) <= TOL, (name, "trace", i)
