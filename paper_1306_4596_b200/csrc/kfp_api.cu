@@ -1522,6 +1522,10 @@ kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter) {
         set_err("kfp_swr_iterate: %d + %d iterations exceed K_max=%d", pb->k_done, n_iter, pb->K_max);
         return KFP_E_STATE;
     }
+    if (pb->chunk_next != 0) {
+        set_err("kfp_swr_iterate: a chunked iteration is in progress (next chunk %d of %d)", pb->chunk_next, pb->nchunks);
+        return KFP_E_STATE;
+    }
     KFP_CUDA(cudaSetDevice(pb->device));
     const int need = 2 + 2 * n_iter;
     while ((int)pb->ev.size() < need) {

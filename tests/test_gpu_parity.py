@@ -215,6 +215,10 @@ def test_block_split_chunked_exchange(kfp, nchunks):
         assert np.array_equal((A if s < 8 else B).subdomain_uT(s), full["uT_sub"][s]), s
     with pytest.raises(kfp.KfpError):  # chunks out of order
         A.iterate_chunk(1, 4)
+    A.reset()
+    A.iterate_chunk(0, 4)
+    with pytest.raises(kfp.KfpError):  # a whole iteration while a chunked one is in progress
+        A.iterate(1)
     A.close()
     B.close()
 
