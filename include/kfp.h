@@ -169,7 +169,8 @@ kfp_status kfp_swr_set_initial_trace(kfp_problem pb, int32_t i, int32_t dir, con
  * subdomain solves the whole window [0,T] from u0 with the previous
  * iteration's traces, writes its outgoing traces and accumulates its errors;
  * local interfaces are exchanged on the device).  Asynchronous on the
- * problem's stream.  KFP_E_STATE if more than K_max iterations in total. */
+ * problem's stream.  KFP_E_STATE if more than K_max iterations in total, or while a chunked iteration
+ * (kfp_swr_iterate_chunk) is in progress. */
 kfp_status kfp_swr_iterate(kfp_problem pb, int32_t n_iter);
 
 /* Time-chunked Jacobi iteration for overlapping the cross-GPU trace exchange with compute (step n
