@@ -296,6 +296,29 @@ def test_sharded_monodomain_reference(kfp, nv):
         torch.cuda.set_stream(torch.cuda.default_stream())
 
 
+@pytest.mark.parametrize("k", [1, 37])
+def test_x_translation_equivariance_full_width(kfp, k):
+    """A property that holds at any size: rolling the x-tables of f and u0 by k columns rolls
+    every output by k columns, bitwise -- configs[2]'s full 4096-column width and its 2048-row subdomains (the
+    production launch plan), window cut to 20 steps.  k = 37 moves every column to another lane, tile and cluster
+    and across the periodic wrap."""
+    import dataclasses
+
+    run = ki.scaled(ki.config("c2"), nt=20, K=2, t_final=0.05 * 20 / 1000, name="c2_roll")
+    prob = ki.make_problem(run)
+    rolled = dataclasses.replace(prob, fx=np.roll(prob.fx, k, axis=1), u0x=np.roll(prob.u0x, k, axis=1))
+    with kfp.Problem(prob) as pa, kfp.Problem(rolled) as pb_:
+        ua = pa.solve(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        ub = pb_.solve(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        ha, hb = pa.history(), pb_.history()
+        ta = [pa.trace(0, d) for d in (0, 1)]
+        tb = [pb_.trace(0, d) for d in (0, 1)]
+    assert np.array_equal(np.roll(ua, k, axis=1), ub)
+    assert np.array_equal(ha[0], hb[0]) and np.array_equal(ha[1], hb[1])
+    for x, y in zip(ta, tb):
+        assert np.array_equal(np.roll(x, k, axis=1), y)
+
+
 def test_c2_full_size_vs_mode_reduced_oracle(kfp):
     """BASELINE.json configs[2] at full size (the bench workload, same launch plan), against the
     mode-reduced oracle (exact for the manufactured data, oracle/modal.py): every output element."""

@@ -404,3 +404,23 @@ def test_survey_scratch_histories_modal(name):
     v = -g.vmax + np.arange(g.nv + 1) * (2 * g.vmax / g.nv)
     c_ex = math.exp(-g.t_final) * (g.vmax ** 2 - v ** 2)
     _check_scratch(_gold(name), max_abs_real(m["C"], g.nx), max_abs_real(m["C"] - c_ex, g.nx), m["err_T"], m["err_if"])
+
+
+def test_x_translation_equivariance(orc):
+    """Every operator of the scheme commutes with x-translation (periodic x, upwind by a column, the v-solve per
+    column): rolling the x-tables of f and u0 by k columns rolls the monodomain solution, every
+    subdomain iterate and the traces by k columns.  Per-column arithmetic is identical, so the identity is
+    bitwise; a transposed or mis-shifted transport stencil breaks it."""
+    import dataclasses
+
+    run = ki.scaled(ki.config("c4"), nx=24, nv=48, nt=12, K=3).with_(n_sub=3, overlap=2)
+    prob = ki.make_problem(run)
+    k = 5
+    rolled = dataclasses.replace(prob, fx=np.roll(prob.fx, k, axis=1), u0x=np.roll(prob.u0x, k, axis=1))
+    a = orc.swr(prob, run.kind, run.p, run.overlap, run.n_sub, run.K, want_traces=True)
+    b = orc.swr(rolled, run.kind, run.p, run.overlap, run.n_sub, run.K, want_traces=True)
+    assert np.array_equal(np.roll(a["UT"], k, axis=1), b["UT"])
+    assert np.array_equal(np.roll(a["uT"], k, axis=1), b["uT"])
+    assert np.array_equal(np.roll(a["traces"], k, axis=2), b["traces"])
+    assert np.array_equal(a["err_T"], b["err_T"]) and np.array_equal(a["err_if"], b["err_if"])
+    assert not np.array_equal(a["UT"], b["UT"])  # control: the roll does change the solution
