@@ -28,3 +28,16 @@ def test_bench_json_line_contract():
     assert roof["bound"] == "hbm" and 0 < roof["frac"] < 1.5 and roof["peak"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert set(d["e2e"]["phases_ms"]) == {"create", "setup_incl_monodomain", "iterate", "d2h", "destroy"}
+
+
+def test_iteration_log_cli():
+    """python -m paper_1306_4596_b200: one JSON line per Jacobi iteration (SURVEY §5 metrics / logging)."""
+    cmd = [sys.executable, "-m", "paper_1306_4596_b200", "--workload", "c0", "--K", "5"]
+    r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert lines[0]["workload"] == "c0" and lines[0]["plan"]
+    its = [x for x in lines if "k" in x]
+    assert [x["k"] for x in its] == [1, 2, 3, 4, 5]
+    assert all(x["ms"] > 0 and x["err_T"] > 0 and x["err_if"] > 0 for x in its)
+    assert lines[-1]["summary"] and lines[-1]["updates_per_s"] > 0
