@@ -103,6 +103,11 @@ CASES = {
     # subdomains of 1029 rows with 4-cell overlap, random f >= 0), small x-extent and window
     "c3_columns": ki.scaled(ki.config("c3"), nx=64, nt=16, K=2, t_final=0.02 * 16 / 1000 * 8, name="c3_columns"),
     "c4_columns": ki.scaled(ki.config("c4"), nx=64, nt=16, K=3, name="c4_columns"),
+    # degenerate sizes: the smallest x-extent (2 columns, one partial tile), 4 subdomains of 3 cells (the fewest
+    # kfp_swr_setup accepts: 3-4 unknown rows each), a one-step window, and a single iteration
+    "tiny_nx2_S4": ki.scaled(ki.config("c0"), nx=2, nv=12, nt=3, K=3, t_final=0.0075, name="tiny").with_(n_sub=4),
+    "one_step_window": ki.scaled(ki.config("c0"), nt=1, K=2, t_final=0.0025, name="one_step"),
+    "one_iteration_dir": ki.scaled(ki.config("c1"), nx=64, nt=30, K=1, name="one_iter"),
     # columns taller than one cluster -> three-phase path
     "three_phase": ki.scaled(ki.config("c2"), nx=64, nv=4400, nt=40, K=3, name="three_phase").with_(n_sub=1),
 }
