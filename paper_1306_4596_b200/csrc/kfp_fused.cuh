@@ -364,6 +364,9 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
 #pragma unroll
     for (int qq = 4; qq < 6; ++qq) cta_special |= inblk(sp_row[qq]);
     const int t_first = P.tile0 + blockIdx.y;  // (a sharded monodomain starts at tile0; ntiles = its end)
+    // x-tile of walk index tt: odd steps walk the tiles in reverse, so that a step first reads the tiles the
+    // previous step wrote last (still in L2)
+    auto phys = [&](int tt) { return (step & 1) ? P.tile0 + FP.ntiles - 1 - tt : tt; };
     const uint32_t tile_bytes = static_cast<uint32_t>(kTW * (L + 2 * kX) * sizeof(double));
     // tensor-map row of the tile's first row: FD maps start at the first unknown row, FEM maps at the
     // slab's first node (the row above the chunk may be a Dirichlet end node)
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
     }
     grid_dep_wait();  // the previous step's u^n is complete
     if (Lw > 0 && !from_u0 && lane == 0 && t_first < FP.ntiles)
-        tma_load_2d(tile_w, tmap, t_first * kWarp - kHalo, ty0, &sm.bar[warp]);
+        tma_load_2d(tile_w, tmap, phys(t_first) * kWarp - kHalo, ty0, &sm.bar[warp]);
     cluster_wait();  // matches the prologue arrive
     KFP_T(1)
 
@@ -410,7 +413,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
     int it = 0;
     for (int t = t_first; t < FP.ntiles; t += FP.Gc, ++it) {
         const int par = it & 1;
-        const int m0 = t * kWarp, w = min(kWarp, P.nx - m0);
+        const int m0 = phys(t) * kWarp, w = min(kWarp, P.nx - m0);
         const int m = m0 + min(lane, w - 1);
         const bool active = lane < w;
         const size_t goff = static_cast<size_t>(step) * P.nx + m;  // row t_{n+1} of [nt][nx] arrays
@@ -510,7 +513,7 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
             if (lane == 0 && !from_u0 && t + FP.Gc < FP.ntiles) {
                 fence_proxy_async_smem();
                 mbar_expect_tx(&sm.bar[warp], tile_bytes);
-                tma_load_2d(tile_w, tmap, (t + FP.Gc) * kWarp - kHalo, ty0, &sm.bar[warp]);
+                tma_load_2d(tile_w, tmap, phys(t + FP.Gc) * kWarp - kHalo, ty0, &sm.bar[warp]);
             }
             if (full) {
                 kst = pass_b_full<B>(h, q);
