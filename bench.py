@@ -260,15 +260,20 @@ def bench_single(args):
     uT_pinned = torch.empty((g.nv + 1, g.nx), dtype=torch.float64, pin_memory=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     d2h = 0
-    for it_ in range(e2e_steps + (1 if e2e_steps else 0)):  # one untimed warm-up solve through the same calls
-        if it_ == 1:
-            torch.cuda.synchronize()
-            e0.record(stream)
+
+    def e2e_solve():
         with Problem(prob_pinned, device=dev) as q:
             q.set_stream(stream.cuda_stream)
             uT = q.solve(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q, out=uT_pinned.numpy())
             h = q.history()
-            d2h = uT.nbytes + h[0].nbytes + h[1].nbytes
+        return uT.nbytes + h[0].nbytes + h[1].nbytes
+
+    if e2e_steps:
+        e2e_solve()  # one untimed warm-up solve through the same calls
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        d2h = e2e_solve()
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / max(1, e2e_steps)

@@ -263,9 +263,6 @@ struct kfp_problem_s {
     double *d_blkagg = nullptr, *d_chkagg = nullptr, *d_carry = nullptr;
     FusedData fd;                    // fused-kernel tensor maps and tables of the SWR setup
     std::vector<double *> swr_allocs;
-#ifdef KFP_L2P_MB
-    cudaAccessPolicyWindow l2win = {};  // experiment: persisting-L2 window over the slab arena
-#endif
     double *edge_sendL[2] = {nullptr, nullptr}, *edge_recvL[2] = {nullptr, nullptr};
     double *edge_sendR[2] = {nullptr, nullptr}, *edge_recvR[2] = {nullptr, nullptr};
     std::vector<double *> zero_on_reset;  // parity-0 incoming buffers
@@ -500,15 +497,6 @@ kfp_status launch_step(kfp_problem pb, const Plan &pl, StepParams &P, int nsub, 
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 2;
-#ifdef KFP_L2P_MB
-        cudaLaunchAttribute attr3[3] = {attr[0], attr[1]};
-        if (pb->l2win.num_bytes) {
-            attr3[2].id = cudaLaunchAttributeAccessPolicyWindow;
-            attr3[2].val.accessPolicyWindow = pb->l2win;
-            cfg.attrs = attr3;
-            cfg.numAttrs = 3;
-        }
-#endif
         KFP_CUDA(cudaLaunchKernelEx(&cfg, k, FP));
         pb->launches += 1;
     } else {
@@ -1335,40 +1323,12 @@ kfp_status swr_setup_impl(kfp_problem pb, kfp_kind kind, const double *ps, const
     if (kfp_status st = configure_kernels(pl)) return st;
 
     // slabs and traces (each replica its own chain of interfaces)
-#ifdef KFP_L2P_MB
-    {
-        size_t tot = 0;
-        for (int ii = 0; ii < ntot; ++ii) tot += 2 * (((size_t)(pb->subs[ii].hi - pb->subs[ii].lo + 1) * nx + 31) / 32 * 32);
-        double *arena = nullptr;
-        if (kfp_status st = swr_alloc(pb, &arena, tot)) return st;
-        size_t off = 0;
-        for (int q = 0; q < 2; ++q)
-            for (int ii = 0; ii < ntot; ++ii) {
-                SubDev &sd = pb->subs[ii];
-                sd.slab[q] = arena + off;
-                off += ((size_t)(sd.hi - sd.lo + 1) * nx + 31) / 32 * 32;
-            }
-        cudaDeviceProp prop;
-        KFP_CUDA(cudaGetDeviceProperties(&prop, pb->device));
-        const size_t want = (size_t)KFP_L2P_MB << 20, persist = std::min(want, (size_t)prop.persistingL2CacheMaxSize);
-        KFP_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
-        const size_t win = std::min(tot * sizeof(double), (size_t)prop.accessPolicyMaxWindowSize);
-        pb->l2win.base_ptr = arena;
-        pb->l2win.num_bytes = win;
-        pb->l2win.hitRatio = (float)std::min(1.0, (double)persist / (double)win);
-        pb->l2win.hitProp = cudaAccessPropertyPersisting;
-        pb->l2win.missProp = cudaAccessPropertyNormal;
-        fprintf(stderr, "l2persist: persist %zu MB (max %d), window %zu MB (max %d), hitRatio %.3f\n", persist >> 20,
-                prop.persistingL2CacheMaxSize >> 20, win >> 20, prop.accessPolicyMaxWindowSize >> 20, pb->l2win.hitRatio);
-    }
-#else
     for (int ii = 0; ii < ntot; ++ii) {
         SubDev &sd = pb->subs[ii];
         const size_t rows = (size_t)(sd.hi - sd.lo + 1);
         for (int q = 0; q < 2; ++q)
             if (kfp_status st = swr_alloc(pb, &sd.slab[q], rows * nx)) return st;
     }
-#endif
     for (int rr = 0; rr < n_rep; ++rr) {
         std::vector<double *> toL(2 * std::max(0, nloc - 1)), toR(2 * std::max(0, nloc - 1));
         for (int i = 0; i + 1 < nloc; ++i)
