@@ -109,8 +109,15 @@ kfp_status kfp_problem_create(const kfp_problem_desc *desc, kfp_problem *out);
  * subdomain and in the monodomain), else the setup / monodomain call returns KFP_E_INVAL. */
 kfp_status kfp_problem_create_ex(const kfp_problem_desc *desc, kfp_scheme scheme, kfp_problem *out);
 
-/* Free every device buffer and the handle (NULL is a no-op). */
+/* Release the handle and its device buffers (NULL is a no-op).  The buffers go to a process-wide cache
+ * keyed by (device, size) after a device synchronisation, and the next problem of the same shape reuses
+ * them instead of calling cudaMalloc (cudaFree of a large problem costs milliseconds to ~0.1 s).  An
+ * allocation that fails for lack of memory first returns that device's cached buffers to the driver. */
 void kfp_problem_destroy(kfp_problem pb);
+
+/* Return every cached device buffer (see kfp_problem_destroy) to the CUDA driver, e.g. before another
+ * library needs the memory.  Safe to call at any time; problems that are alive are not affected. */
+void kfp_release_cached_memory(void);
 
 /* Run all subsequent work on `stream` (a cudaStream_t on the problem's
  * device, e.g. torch.cuda.current_stream().cuda_stream); NULL restores the

@@ -13,7 +13,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <cuda.h>
@@ -28,6 +31,113 @@ using kfp::StepParams;
 
 namespace {
 thread_local std::string g_err;
+
+// Process-wide cache of device buffers keyed by (device, bytes).  A destroyed problem's buffers serve the next
+// problem of the same shape: cudaFree of the ~0.7 GB of a c2 problem cost 4-130 ms per destroy (it synchronises
+// the device and unmaps), which made the end-to-end solve time vary by 25 %.  "Freeing" synchronises the device
+// (as cudaFree did) and parks the buffer; an allocation that finds no parked buffer of its size calls cudaMalloc,
+// and on out-of-memory releases the parked buffers of the device and retries.  kfp_release_cached_memory()
+// returns everything to the driver.
+struct DevCache {
+    std::mutex mu;
+    std::multimap<std::pair<int, size_t>, void *> parked;
+    std::unordered_map<void *, std::pair<int, size_t>> live;
+    size_t parked_bytes = 0;
+};
+DevCache &dcache() {
+    static DevCache *c = new DevCache();  // never destroyed: buffers may be freed from static destructors
+    return *c;
+}
+constexpr size_t kCacheCapBytes = size_t(32) << 30;
+
+void release_parked(int dev_only) {  // dev_only < 0: every device (caller holds no lock)
+    std::vector<std::pair<int, void *>> drop;
+    {
+        DevCache &c = dcache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto it = c.parked.begin(); it != c.parked.end();) {
+            if (dev_only < 0 || it->first.first == dev_only) {
+                drop.emplace_back(it->first.first, it->second);
+                c.parked_bytes -= it->first.second;
+                it = c.parked.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto &d : drop) {
+        cudaSetDevice(d.first);
+        cudaFree(d.second);
+    }
+    cudaSetDevice(cur);
+}
+
+cudaError_t dev_malloc_raw(void **p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    bytes = (std::max<size_t>(bytes, 1) + 255) / 256 * 256;
+    const auto key = std::make_pair(dev, bytes);
+    DevCache &c = dcache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.parked.find(key);
+        if (it != c.parked.end()) {
+            *p = it->second;
+            c.parked.erase(it);
+            c.parked_bytes -= bytes;
+            c.live[*p] = key;
+            return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        release_parked(dev);
+        e = cudaMalloc(p, bytes);
+    }
+    if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.live[*p] = key;
+    }
+    return e;
+}
+template <class T>
+cudaError_t dev_malloc(T **p, size_t bytes) {
+    void *v = nullptr;
+    const cudaError_t e = dev_malloc_raw(&v, bytes);
+    *p = static_cast<T *>(v);
+    return e;
+}
+cudaError_t dev_free(void *p) {
+    if (!p) return cudaSuccess;
+    DevCache &c = dcache();
+    std::pair<int, size_t> key;
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.live.find(p);
+        if (it == c.live.end()) return cudaFree(p);
+        key = it->second;
+        c.live.erase(it);
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != key.first) cudaSetDevice(key.first);
+    cudaDeviceSynchronize();  // no kernel or copy of the old owner still uses it (cudaFree's own semantics)
+    cudaError_t e = cudaSuccess;
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (c.parked_bytes + key.second <= kCacheCapBytes) {
+            c.parked.emplace(key, p);
+            c.parked_bytes += key.second;
+            p = nullptr;
+        }
+    }
+    if (p) e = cudaFree(p);
+    if (cur != key.first) cudaSetDevice(cur);
+    return e;
+}
 
 void set_err(const char *fmt, ...) {
     char buf[512];
@@ -284,21 +394,21 @@ namespace {
 template <class T>
 kfp_status dalloc(kfp_problem pb, T **p, size_t count, std::vector<void *> *list = nullptr) {
     void *q = nullptr;
-    KFP_CUDA(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T)));
+    KFP_CUDA(dev_malloc(&q, std::max<size_t>(count, 1) * sizeof(T)));
     *p = static_cast<T *>(q);
     (list ? *list : pb->allocs).push_back(q);
     return KFP_OK;
 }
 
 void free_swr(kfp_problem pb) {
-    for (double *p : pb->swr_allocs) cudaFree(p);
+    for (double *p : pb->swr_allocs) dev_free(p);
     pb->swr_allocs.clear();
     pb->subs.clear();
     pb->zero_on_reset.clear();
-    if (pb->d_subs) cudaFree(pb->d_subs);
+    if (pb->d_subs) dev_free(pb->d_subs);
     pb->d_subs = nullptr;
-    if (pb->d_errT) cudaFree(pb->d_errT);
-    if (pb->d_errIF) cudaFree(pb->d_errIF);
+    if (pb->d_errT) dev_free(pb->d_errT);
+    if (pb->d_errIF) dev_free(pb->d_errIF);
     pb->d_errT = pb->d_errIF = nullptr;
     pb->d_errOV = nullptr;  // (in swr_allocs)
     pb->d_pairs = nullptr;
@@ -321,7 +431,7 @@ void free_swr(kfp_problem pb) {
 
 kfp_status swr_alloc(kfp_problem pb, double **p, size_t count) {
     void *q = nullptr;
-    KFP_CUDA(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(double)));
+    KFP_CUDA(dev_malloc(&q, std::max<size_t>(count, 1) * sizeof(double)));
     *p = static_cast<double *>(q);
     pb->swr_allocs.push_back(*p);
     return KFP_OK;
@@ -576,7 +686,7 @@ kfp_status build_l2m(kfp_problem pb, const Plan &pl, const std::vector<SubDev> &
         }
     }
     void *d = nullptr;
-    KFP_CUDA(cudaMalloc(&d, sizeof(double) * h.size()));
+    KFP_CUDA(dev_malloc(&d, sizeof(double) * h.size()));
     KFP_CUDA(cudaMemcpy(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
     *out = static_cast<double *>(d);
     if (owner) owner->push_back(d);
@@ -621,9 +731,9 @@ kfp_status build_fused_tables(kfp_problem pb, const Plan &pl, std::vector<double
     t[2 * kQ + 2 * pl.B + 2] = (double)powl(q, pl.L + 1);
     t[2 * kQ + 2 * pl.B + 3] = (double)powl(q, pl.L);
     void *d1 = nullptr, *d2 = nullptr;
-    KFP_CUDA(cudaMalloc(&d1, sizeof(double) * c.size()));
+    KFP_CUDA(dev_malloc(&d1, sizeof(double) * c.size()));
     KFP_CUDA(cudaMemcpy(d1, c.data(), sizeof(double) * c.size(), cudaMemcpyHostToDevice));
-    KFP_CUDA(cudaMalloc(&d2, sizeof(double) * t.size()));
+    KFP_CUDA(dev_malloc(&d2, sizeof(double) * t.size()));
     KFP_CUDA(cudaMemcpy(d2, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice));
     *coefT = static_cast<double *>(d1);
     *tabs = static_cast<double *>(d2);
@@ -654,7 +764,7 @@ kfp_status build_tmaps(kfp_problem pb, const Plan &pl, const std::vector<SubDev>
             }
         }
     void *d = nullptr;
-    KFP_CUDA(cudaMalloc(&d, sizeof(CUtensorMap) * maps.size()));
+    KFP_CUDA(dev_malloc(&d, sizeof(CUtensorMap) * maps.size()));
     KFP_CUDA(cudaMemcpy(d, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
     *out = static_cast<CUtensorMap *>(d);
     if (owner) owner->push_back(d);
@@ -693,7 +803,7 @@ kfp_status alloc_general_scratch(kfp_problem pb, const Plan &pl, int nsub, doubl
     const size_t nx = pb->nx;
     auto al = [&](double **p, size_t c) -> kfp_status {
         void *q = nullptr;
-        KFP_CUDA(cudaMalloc(&q, std::max<size_t>(c, 1) * sizeof(double)));
+        KFP_CUDA(dev_malloc(&q, std::max<size_t>(c, 1) * sizeof(double)));
         *p = static_cast<double *>(q);
         owner.push_back(*p);
         return KFP_OK;
@@ -747,7 +857,7 @@ kfp_status mono_begin(kfp_problem pb, const std::vector<int> &lines, int x0, int
     KFP_CUDA(cudaMemcpyAsync(pb->d_line_of_node, lon.data(), nn * sizeof(int), cudaMemcpyHostToDevice, pb->stream));
     KFP_CUDA(cudaStreamSynchronize(pb->stream));  // (lon is a host temporary)
     if (pb->d_Ulines) {
-        cudaFree(pb->d_Ulines);
+        dev_free(pb->d_Ulines);
         pb->allocs.erase(std::find(pb->allocs.begin(), pb->allocs.end(), (void *)pb->d_Ulines));
         pb->d_Ulines = nullptr;
     }
@@ -808,7 +918,7 @@ kfp_status mono_begin(kfp_problem pb, const std::vector<int> &lines, int x0, int
     }
     if (kfp_status st = ensure_qtab(pb, std::max(pl.R, nmax) + 2)) return st;
     if (kfp_status st = configure_kernels(pl)) return st;
-    KFP_CUDA(cudaMalloc(&mr.d_sd, sizeof(SubDev) * mr.segs.size()));
+    KFP_CUDA(dev_malloc(&mr.d_sd, sizeof(SubDev) * mr.segs.size()));
     KFP_CUDA(cudaMemcpyAsync(mr.d_sd, mr.segs.data(), sizeof(SubDev) * mr.segs.size(), cudaMemcpyHostToDevice, pb->stream));
     StepParams &P = mr.P;
     P = base_params(pb);
@@ -825,7 +935,7 @@ kfp_status mono_begin(kfp_problem pb, const std::vector<int> &lines, int x0, int
     if (!st) st = build_l2m(pb, pl, mr.segs, &mr.fd.l2c, &mr.tmp2);
     if (!st) st = build_fused_tables(pb, pl, &pb->fv_host, &mr.fd.coefT, &mr.fd.tabs, &mr.tmp2);
     if (!st && !mr.rec_rows.empty()) {
-        if (cudaMalloc(&mr.d_rec, sizeof(int) * mr.rec_rows.size()) != cudaSuccess ||
+        if (dev_malloc(&mr.d_rec, sizeof(int) * mr.rec_rows.size()) != cudaSuccess ||
             cudaMemcpy(mr.d_rec, mr.rec_rows.data(), sizeof(int) * mr.rec_rows.size(), cudaMemcpyHostToDevice) != cudaSuccess)
             st = KFP_E_CUDA;
     }
@@ -841,10 +951,10 @@ kfp_status mono_begin(kfp_problem pb, const std::vector<int> &lines, int x0, int
 
 void mono_free(kfp_problem pb) {
     MonoRun &mr = pb->mr;
-    if (mr.d_sd) cudaFree(mr.d_sd);
-    if (mr.d_rec) cudaFree(mr.d_rec);
-    for (double *q : mr.tmp) cudaFree(q);
-    for (void *q : mr.tmp2) cudaFree(q);
+    if (mr.d_sd) dev_free(mr.d_sd);
+    if (mr.d_rec) dev_free(mr.d_rec);
+    for (double *q : mr.tmp) dev_free(q);
+    for (void *q : mr.tmp2) dev_free(q);
     mr = MonoRun();
 }
 
@@ -908,6 +1018,8 @@ kfp_status run_monodomain(kfp_problem pb, const std::vector<int> &lines) {
 extern "C" {
 
 const char *kfp_last_error(void) { return g_err.c_str(); }
+
+void kfp_release_cached_memory(void) { release_parked(-1); }
 
 kfp_status kfp_problem_create(const kfp_problem_desc *d, kfp_problem *out) {
     return kfp_problem_create_ex(d, KFP_SCHEME_IMEX_FD, out);
@@ -1035,7 +1147,7 @@ void kfp_problem_destroy(kfp_problem pb) {
     if (pb->stream) cudaStreamSynchronize(pb->stream);
     if (pb->mr.active) mono_free(pb);
     free_swr(pb);
-    for (void *p : pb->allocs) cudaFree(p);
+    for (void *p : pb->allocs) dev_free(p);
     for (cudaEvent_t e : pb->ev) cudaEventDestroy(e);
     for (cudaEvent_t e : pb->chunk_sent) cudaEventDestroy(e);
     for (cudaEvent_t e : pb->chunk_recv) cudaEventDestroy(e);
@@ -1371,13 +1483,13 @@ kfp_status swr_setup_impl(kfp_problem pb, kfp_kind kind, const double *ps, const
         }
     {
         void *q = nullptr;
-        KFP_CUDA(cudaMalloc(&q, sizeof(SubDev) * ntot));
+        KFP_CUDA(dev_malloc(&q, sizeof(SubDev) * ntot));
         pb->d_subs = static_cast<SubDev *>(q);
-        KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max * n_rep));
+        KFP_CUDA(dev_malloc(&q, sizeof(unsigned long long) * K_max * n_rep));
         pb->d_errT = static_cast<unsigned long long *>(q);
-        KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max * n_rep));
+        KFP_CUDA(dev_malloc(&q, sizeof(unsigned long long) * K_max * n_rep));
         pb->d_errIF = static_cast<unsigned long long *>(q);
-        KFP_CUDA(cudaMalloc(&q, sizeof(unsigned long long) * K_max * n_rep));
+        KFP_CUDA(dev_malloc(&q, sizeof(unsigned long long) * K_max * n_rep));
         pb->d_errOV = static_cast<unsigned long long *>(q);
         pb->swr_allocs.push_back(reinterpret_cast<double *>(pb->d_errOV));
     }
@@ -1804,7 +1916,7 @@ kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth) {
     std::vector<double *> fresh;  // this call's allocations (freed if it fails)
     auto al = [&](double **p, size_t count) -> kfp_status {
         void *q = nullptr;
-        if (cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(double)) != cudaSuccess) {
+        if (dev_malloc(&q, std::max<size_t>(count, 1) * sizeof(double)) != cudaSuccess) {
             cudaGetLastError();
             set_err("kfp_swr_set_pipeline: device allocation of %zu doubles failed", count);
             return KFP_E_NOMEM;
@@ -1814,7 +1926,7 @@ kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth) {
         return KFP_OK;
     };
     auto fail = [&](kfp_status st) {
-        for (double *p : fresh) cudaFree(p);
+        for (double *p : fresh) dev_free(p);
         return st;
     };
     // trace rings: slots 0 and 1 are the setup's parity buffers (slot 0 is what reset / set_initial_trace write)
@@ -1921,7 +2033,7 @@ kfp_status kfp_swr_set_overlap_error(kfp_problem pb, int32_t on) {
         }
     if (!pairs.empty()) {
         void *q = nullptr;
-        KFP_CUDA(cudaMalloc(&q, sizeof(int2) * pairs.size()));
+        KFP_CUDA(dev_malloc(&q, sizeof(int2) * pairs.size()));
         pb->d_pairs = static_cast<int2 *>(q);
         pb->swr_allocs.push_back(static_cast<double *>(q));
         KFP_CUDA(cudaMemcpy(pb->d_pairs, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice));
@@ -2149,7 +2261,7 @@ int64_t kfp_launch_count(kfp_problem pb) { return pb ? pb->launches : -1; }
 // debug builds only (not part of include/kfp.h): one traced step launch of the current setup
 extern "C" int kfp_debug_trace_step(kfp_problem pb, int n, unsigned long long *host, int cap) {
     unsigned long long *d = nullptr;
-    cudaMalloc(&d, sizeof(unsigned long long) * cap * 64);
+    dev_malloc(&d, sizeof(unsigned long long) * cap * 64);
     cudaMemset(d, 0, sizeof(unsigned long long) * cap * 64);
     cudaMemcpyToSymbol(kfp::g_kfp_trace, &d, sizeof(d));
     StepParams P = base_params(pb);
@@ -2170,7 +2282,7 @@ extern "C" int kfp_debug_trace_step(kfp_problem pb, int n, unsigned long long *h
     unsigned long long *z = nullptr;
     cudaMemcpyToSymbol(kfp::g_kfp_trace, &z, sizeof(z));
     cudaMemcpy(host, d, sizeof(unsigned long long) * cap * 64, cudaMemcpyDeviceToHost);
-    cudaFree(d);
+    dev_free(d);
     return (int)cudaGetLastError();
 }
 #endif

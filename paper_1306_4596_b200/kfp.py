@@ -26,7 +26,7 @@ SYMBOLS = (
     "kfp_swr_batch_history", "kfp_swr_batch_subdomain_uT", "kfp_swr_set_initial_trace",
     "kfp_swr_reset", "kfp_swr_iterate", "kfp_swr_edge_buffers", "kfp_swr_bind_edge_buffers", "kfp_swr_solve", "kfp_error_history",
     "kfp_swr_subdomain_uT", "kfp_swr_subdomain_range", "kfp_swr_trace", "kfp_monodomain_uT", "kfp_launch_count",
-    "kfp_plan", "kfp_last_timing", "kfp_last_error",
+    "kfp_plan", "kfp_last_timing", "kfp_last_error", "kfp_release_cached_memory",
     "kfp_swr_set_overlap_error", "kfp_swr_overlap_history", "kfp_swr_iterate_until", "kfp_swr_set_pipeline",
     "kfp_swr_iterate_chunk", "kfp_swr_chunk_send_wait", "kfp_swr_chunk_recv_done",
     "kfp_monodomain_shard_begin", "kfp_monodomain_shard_step", "kfp_monodomain_shard_end", "kfp_monodomain_shard_copy",
@@ -94,6 +94,7 @@ def load(path: str = LIB_PATH):
         "kfp_plan": (ctypes.c_char_p, [vp]),
         "kfp_last_timing": (i32, [vp, pd, pd]),
         "kfp_last_error": (ctypes.c_char_p, []),
+        "kfp_release_cached_memory": (None, []),
         "kfp_swr_set_overlap_error": (i32, [vp, i32]),
         "kfp_swr_set_pipeline": (i32, [vp, i32]),
         "kfp_swr_overlap_history": (i32, [vp, i32, i32, ctypes.POINTER(i32), vp]),
@@ -351,3 +352,8 @@ class Problem:
 
 def last_error() -> str:
     return load().kfp_last_error().decode()
+
+
+def release_cached_memory() -> None:
+    """Return the device buffers of destroyed problems (kept for reuse, include/kfp.h) to the CUDA driver."""
+    load().kfp_release_cached_memory()

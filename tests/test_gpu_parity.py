@@ -563,3 +563,31 @@ def test_solve_writes_into_out(kfp):
         res = pb.solve(run.kind, run.p, run.overlap, run.n_sub, run.K, out=out)
     assert res is out
     assert np.array_equal(out, ref)
+
+
+def test_destroyed_buffers_are_reused_bitwise(kfp):
+    """kfp_problem_destroy parks the device buffers for the next problem of the same shape (include/kfp.h):
+    a solve on recycled buffers -- including ones a differently shaped problem used in between, and after
+    kfp_release_cached_memory -- is bitwise the first solve, and a live problem is unaffected by the others."""
+    run = ki.config("c1").with_(K=3)
+    other = ki.config("c0").with_(K=2)
+
+    def solve(r):
+        with kfp.Problem(ki.make_problem(r)) as pb:
+            u = pb.solve(r.kind, r.p, r.overlap, r.n_sub, r.K)
+            return u, pb.history()
+
+    u1, h1 = solve(run)
+    with kfp.Problem(ki.make_problem(run)) as live:  # alive while other problems come and go
+        u_live = live.solve(run.kind, run.p, run.overlap, run.n_sub, run.K)
+        uo1, _ = solve(other)
+        u2, h2 = solve(run)                           # on the buffers of the first solve
+        uo2, _ = solve(other)
+        kfp.release_cached_memory()
+        u3, h3 = solve(run)                           # fresh cudaMalloc again
+        assert np.array_equal(live.solve(run.kind, run.p, run.overlap, run.n_sub, run.K), u_live)
+    for u, h in ((u2, h2), (u3, h3)):
+        assert np.array_equal(u, u1)
+        assert np.array_equal(h[0], h1[0]) and np.array_equal(h[1], h1[1])
+    assert np.array_equal(u_live, u1)
+    assert np.array_equal(uo1, uo2)
