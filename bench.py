@@ -271,9 +271,12 @@ def bench_single(args):
     if e2e_steps:
         e2e_solve()  # one untimed warm-up solve through the same calls
     torch.cuda.synchronize()
+    e2e_host_ms = []
     e0.record(stream)
     for _ in range(e2e_steps):
+        th = time.perf_counter()
         d2h = e2e_solve()
+        e2e_host_ms.append(round((time.perf_counter() - th) * 1e3, 3))
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / max(1, e2e_steps)
@@ -346,7 +349,7 @@ def bench_single(args):
                      "traffic_source": "profiles/*_ncu_summary.json (ncu --set full, same plan)" if traffic else None,
                      "bytes_per_launch": bytes_per_launch, "avg_launch_us": per_launch_s * 1e6},
         "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": pb.h2d_bytes,
-                "d2h_bytes_per_step": int(d2h), "ms": e2e_ms, "phases_ms": phases},
+                "d2h_bytes_per_step": int(d2h), "ms": e2e_ms, "host_ms_per_solve": e2e_host_ms, "phases_ms": phases},
         "monodomain": mono,
         "ms_per_step_median": float(np.median(step_ms)), "ms_per_step_all": [round(x, 3) for x in step_ms],
         "gpu_launches": int(launches),
