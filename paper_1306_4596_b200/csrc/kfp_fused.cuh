@@ -55,16 +55,6 @@ struct FusedParams {
 
 // --------------------------------------------------------------------------- PTX
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
-#ifdef KFP_LD_EVICT_FIRST  // experiment: u^n is dead once this step has read it
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], "
-        "[%4], %5;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-    return;
-#endif
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
         "[%4];" ::"r"(smem_u32(dst)),
@@ -661,20 +651,10 @@ __global__ void __launch_bounds__(P_ * kWarp, 16 / P_) step_fused_tma(const Fuse
                 if (Lw == B && cr0 >= wlo && cr0 + B <= whi) {  // full chunk: unpredicated stores, one pointer step per row
                     double *p = dst;
 #pragma unroll
-#ifdef KFP_ST_EVICT_LAST  // experiment: u^{n+1} is read by the next step
-                    uint64_t spol;
-                    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(spol));
-#pragma unroll
-                    for (int l = 0; l < B; ++l) {
-                        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(h[l]), "l"(spol));
-                        p += pitch;
-                    }
-#else
                     for (int l = 0; l < B; ++l) {
                         st_global_f64(p, h[l]);
                         p += pitch;
                     }
-#endif
                 } else {
 #pragma unroll
                     for (int l = 0; l < B; ++l)
