@@ -248,7 +248,7 @@ def bench_single(args):
 
     # end to end through the public API with host buffers (create -> solve -> read back): the input tables and
     # the result live in pinned host memory (allocated outside the timed region)
-    e2e_steps = 0 if args.no_e2e else max(1, min(args.steps, 2))
+    e2e_steps = 0 if args.no_e2e else max(1, min(args.steps, 5))
 
     def pinned_copy(a):
         t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
