@@ -192,6 +192,7 @@ def bench_single(args):
     pb = Problem(prob, device=dev)
     pb.set_stream(stream.cuda_stream)
     pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)  # monodomain reference here (untimed)
+    pb.set_pipeline(0)  # the library's automatic schedule, as kfp_swr_solve (pipelines only latency-bound windows)
     torch.cuda.synchronize()
 
     def one():
@@ -238,9 +239,12 @@ def bench_single(args):
     # Dirichlet interface ends and (IMEX FD) the physical ends are not solved; the split-FEM scheme's
     # physical ends are Neumann (unknown)
     unknown_rows = rows - 2 * (run.n_sub - 1) * (0 if run.kind == "robin" else 1) - (0 if run.scheme == "split_fem" else 2)
-    step_launches = g.nt * run.K * args.steps
+    # per launch of the step kernel: the launches actually made (a pipelined sweep advances several iterations
+    # per launch; otherwise nt * K per solve) and the algorithmic bytes they moved
+    nominal = g.nt * run.K * args.steps
+    step_launches = launches if 0 < launches < nominal else nominal
     per_launch_s = step_kernel_ms / 1e3 / step_launches
-    bytes_per_launch = BYTES_PER_UPDATE * g.nx * unknown_rows
+    bytes_per_launch = BYTES_PER_UPDATE * g.nx * unknown_rows * nominal / step_launches
     achieved = bytes_per_launch / per_launch_s / 1e9
     peak, peak_kind = measured_peaks()
     traffic = committed_traffic(plan := pb.plan())

@@ -215,7 +215,8 @@ kfp_status kfp_swr_bind_edge_buffers(kfp_problem pb, int32_t parity, double *sen
                                      double *send_right, double *recv_right);
 
 /* Convenience: setup(s_begin=0, s_end=n_sub, K_max=K) + reset + iterate(K) on
- * one process.  uT: host [(nv+1)*nx] receiving u^K(T) assembled by nominal
+ * one process.  A latency-bound problem (e.g. BASELINE configs[0] and [1]) iterates pipelined
+ * (kfp_swr_set_pipeline(pb, 0), automatic depth): the results are bitwise those of the unpipelined schedule.  uT: host [(nv+1)*nx] receiving u^K(T) assembled by nominal
  * ownership (node j from the subdomain s with c_s <= j < c_{s+1}, node nv from
  * n_sub-1), or NULL. */
 kfp_status kfp_swr_solve(kfp_problem pb, kfp_kind kind, double p, int32_t overlap, int32_t n_sub, int32_t K,
@@ -283,7 +284,10 @@ kfp_status kfp_swr_overlap_history(kfp_problem pb, int32_t rep, int32_t cap, int
  * direction.  depth >= 2 needs a fresh setup (call right after setup / reset), every subdomain on this
  * process, the per-step cluster kernel and no overlap recording -> else KFP_E_INVAL / KFP_E_STATE.
  * kfp_swr_iterate then runs in groups of <= depth iterations (one host synchronisation per group);
- * kfp_last_timing reports per-group windows. */
+ * kfp_last_timing reports per-group windows.  depth 0 = automatic: a latency-bound problem (one step launch
+ * fills at most half of the GPU's co-resident cluster slots) gets depth min(K_max, 16, slots / clusters per
+ * step), any other problem stays unpipelined; returns KFP_OK without a change where pipelining does not
+ * apply (kfp_swr_solve uses this). */
 kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth);
 
 /* Tolerance stopping: run iterations until `metric` of one of them (replica 0) is below eps,

@@ -1872,10 +1872,27 @@ kfp_status kfp_swr_chunk_recv_done(kfp_problem pb, void *stream, int32_t chunk) 
     return KFP_OK;
 }
 
+// Automatic depth (kfp_swr_set_pipeline(pb, 0)): latency-bound problems -- one step launch occupies at most
+// half of the co-resident cluster slots, e.g. the small windows of BASELINE configs[0] and [1] -- get up to
+// min(K_max, 16) iterations per sweep; a problem that fills the GPU keeps 1.
+static int auto_pipeline_depth(kfp_problem pb) {
+    const Plan &pl = pb->plan;
+    if (!pl.fused || pb->ovrec) return 1;
+    const int nsub = std::max(1, (int)pb->subs.size());
+    const int ntiles = (pb->nx + kfp::kWarp - 1) / kfp::kWarp;
+    const int per_launch = std::max(1, std::min(ntiles, pl.Gc_total / nsub)) * nsub;  // clusters of one step
+    return std::max(1, std::min({pb->K_max, 16, pl.Gc_total / per_launch}));
+}
+
 kfp_status kfp_swr_set_pipeline(kfp_problem pb, int32_t depth) {
     if (!pb || !pb->setup) {
         set_err("kfp_swr_set_pipeline: no setup");
         return KFP_E_STATE;
+    }
+    if (depth == 0) {
+        if (pb->k_done != 0 || pb->pipe != 1) return KFP_OK;  // automatic: only on a fresh unpipelined setup
+        depth = auto_pipeline_depth(pb);
+        if (depth < 2) return KFP_OK;
     }
     if (depth < 1 || depth > 64) {
         set_err("kfp_swr_set_pipeline: depth %d outside [1, 64]", depth);
@@ -2176,6 +2193,7 @@ kfp_status kfp_swr_solve_pq(kfp_problem pb, kfp_kind kind, double p, double q, i
                             int32_t K, double *uT) {
     if (kfp_status st = kfp_swr_setup_pq(pb, kind, p, q, overlap, n_sub, 0, n_sub, K)) return st;
     std::string warn = g_err;
+    kfp_swr_set_pipeline(pb, 0);  // latency-bound problems: pipelined iterations (on failure: unchanged)
     if (kfp_status st = kfp_swr_iterate(pb, K)) return st;
     if (uT) {
         const size_t nx = pb->nx;

@@ -23,7 +23,8 @@ def test_bench_json_line_contract():
         assert k in d, k
     assert d["steps"] == 2 and d["warmup"] == 1 and d["n_gpus"] == 1
     assert d["config"]["workload"] == "c1" and d["dtype"] == "f64"
-    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 2 * 40 * 1000
+    # configs[1] is latency-bound: the automatic schedule pipelines it (fewer launches than nt * K per solve)
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and 0 < d["gpu_launches"] < 2 * 40 * 1000
     roof = d["roofline"]
     assert roof["bound"] == "hbm" and 0 < roof["frac"] < 1.5 and roof["peak"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0

@@ -591,3 +591,37 @@ def test_destroyed_buffers_are_reused_bitwise(kfp):
         assert np.array_equal(h[0], h1[0]) and np.array_equal(h[1], h1[1])
     assert np.array_equal(u_live, u1)
     assert np.array_equal(uo1, uo2)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_solve_schedule_equals_unpipelined(kfp, name):
+    """kfp_swr_solve pipelines latency-bound problems on its own (include/kfp.h); whichever schedule it picks, its
+    slabs, histories and traces are bitwise those of setup + reset + iterate with one iteration per sweep (so the
+    oracle parity of test_parity_vs_oracle holds for both)."""
+    run = CASES[name]
+
+    def collect(pb):
+        eT, eI = pb.history()
+        return ([pb.subdomain_uT(s) for s in range(run.n_sub)], eT, eI,
+                [pb.trace(i, d) for i in range(run.n_sub - 1) for d in (0, 1)])
+
+    prob = ki.make_problem(run)
+    with kfp.Problem(prob) as pa:
+        pa.solve(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q, copy=False)
+        a = collect(pa)
+    with kfp.Problem(prob) as pb:
+        pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
+        pb.reset()
+        pb.iterate(run.K)
+        b = collect(pb)
+    for x, y in zip(a[0] + [a[1], a[2]] + a[3], b[0] + [b[1], b[2]] + b[3]):
+        assert np.array_equal(x, y), name
+
+
+def test_solve_pipelines_small_problems(kfp):
+    """configs[0]: the automatic schedule runs nt + depth - 1 step launches per group of depth iterations."""
+    run = ki.config("c0")
+    with kfp.Problem(ki.make_problem(run)) as pb:
+        pb.solve(run.kind, run.p, run.overlap, run.n_sub, run.K, copy=False)
+        n = pb.launch_count() - run.grid.nt  # minus the monodomain reference
+    assert n < run.grid.nt * run.K // 4, n

@@ -37,8 +37,8 @@ def _solve(kfp, run, depth, lam=None, schedule="jacobi"):
     with kfp.Problem(ki.make_problem(run)) as pb:
         pb.setup(run.kind, run.p, run.overlap, run.n_sub, run.K, q=run.q)
         pb.set_schedule(schedule)
-        if depth > 1:
-            pb.set_pipeline(depth)
+        if depth != 1:
+            pb.set_pipeline(depth)  # 0: the library's automatic depth
         pb.reset()
         if lam is not None:
             for i in range(run.n_sub - 1):
@@ -214,3 +214,22 @@ def test_api_error_paths(kfp):
         pb.reset()  # still usable
         k = pb.iterate_until(0.0, run.K, "err_T")  # eps = 0: never met, runs K_max
         assert k == run.K and len(pb.history()[0]) == run.K
+
+
+def test_automatic_depth(kfp):
+    """set_pipeline(0): a latency-bound window (configs[0]) is pipelined -- bitwise the unpipelined results in
+    fewer launches -- and a window that fills the GPU (configs[2]) is left at one iteration per sweep."""
+    run = RUNS["c0"]
+    a, b = _solve(kfp, run, 1), _solve(kfp, run, 0)
+    assert np.array_equal(a["eT"], b["eT"]) and np.array_equal(a["eI"], b["eI"])
+    for x, y in zip(a["slabs"] + a["traces"], b["slabs"] + b["traces"]):
+        assert np.array_equal(x, y)
+    assert b["launches"] < a["launches"] // 2
+    big = ki.config("c2")
+    with kfp.Problem(ki.make_problem(big)) as pb:
+        pb.setup(big.kind, big.p, big.overlap, big.n_sub, big.K)
+        pb.set_pipeline(0)
+        pb.reset()
+        l0 = pb.launch_count()
+        pb.iterate(1)
+        assert pb.launch_count() - l0 == big.grid.nt
