@@ -209,7 +209,7 @@ def test_api_error_paths(kfp):
             pb.iterate_until(1e-6, run.K, "err_if")
         assert e.value.status == kfp.KFP_E_STATE
         with pytest.raises(kfp.KfpError) as e:
-            pb.set_pipeline(0)
+            pb.set_pipeline(-1)  # (0 = the automatic depth)
         assert e.value.status == kfp.KFP_E_INVAL
         pb.reset()  # still usable
         k = pb.iterate_until(0.0, run.K, "err_T")  # eps = 0: never met, runs K_max
