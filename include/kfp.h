@@ -265,7 +265,7 @@ typedef enum { KFP_ERR_T = 0, KFP_ERR_IF = 1, KFP_ERR_OVERLAP = 2 } kfp_metric;
  * allocates, per local interface and side, (hi_s - lo_{s+1} + 1) * nt * nx doubles of device memory; every
  * step then also stores the subdomains' overlap rows (Dirichlet end nodes from the incoming trace), and
  * every iteration ends with one reduction launch.  KFP_E_STATE before a setup; KFP_E_INVAL unless the plan
- * is the per-step cluster kernel (not KFP_WINDOW / KFP_COL / the three-phase path). */
+ * is the per-step cluster kernel (not the three-phase path of columns above 4224 rows). */
 kfp_status kfp_swr_set_overlap_error(kfp_problem pb, int32_t on);
 
 /* err_ov history of replica `rep` (0 for an ordinary setup): as kfp_error_history.  KFP_E_STATE if the

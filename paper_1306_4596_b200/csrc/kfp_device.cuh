@@ -92,7 +92,7 @@ struct StepParams {
     int ovrec;             // record the overlap rows into SubDev::ovb (cluster kernel only)
     double q, a, qa, hv, dt, p;   // split FEM: a = tau/h_v^2 - 1/6, dt = tau
     double dnu, nu0;       // split FEM transport weight of node j: |j dnu + nu0| = |v_j| tau / h_x (0 at n = 0)
-    double cf[kMaxRank];   // dt * ft[r][n+1]  (window / column kernels)
+    double cf[kMaxRank];   // dt * ft[r][n+1] of this launch's step (the cluster kernel's forcing weights)
     const double *cfn;     // [nt][kMaxRank] dt * ft[r][n+1] per step (cluster kernel: steps differ per slot)
     const double2 *rowc;   // per node: (1-|nu_j|, |nu_j|)
     const double *fv;      // [f_rank][nv+1]
